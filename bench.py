@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the multistep stencil sweep (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
+N=2^26 interior points, T=1000 steps, coefficients (1/16, 1/4, 3/8, 1/4,
+1/16), fixed halo, fusion depth k swept over {1,2,4,8} (default k=8).
+One bench "step" = one full sweep (T=1000 time steps over the whole grid).
+At N>1 GPUs the same workload is weak-scaled: each rank owns a 2^26-point
+slab of a 2^26*N-point line, with an r*k-deep ghost exchange every launch.
+
+Prints ONE JSON line (rank 0).  ``value`` = whole-job GStencil/s with the
+grid resident in HBM (CUDA events on the launching stream, max over ranks);
+``e2e`` = the same metric through the C-ABI call with host buffers (pinned
+H2D of the input grid + sweep + D2H of the output grid, every step).
+
+``--impl reference`` times the reference's algorithm on the host CPU: the
+oracle port (oracle/oracle.c, a bit-exact C+OpenMP restatement of
+stencilbench's scalar oracle -- the reference is pure Python and cannot be
+compiled into oracle/_ref) on all host threads, on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOADS = {
+    "c1": dict(spec="c1", n=1 << 20, T=64, name="1D3P fp64 N=2^20 T=64"),
+    "c2": dict(spec="c2", n=1 << 26, T=1000, name="1D5P fp64 N=2^26 T=1000"),
+}
+ALG_BYTES_PER_POINT = 16          # fp64 read + write once per fused launch
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--arith", default="fma", choices=["fma", "exact"])
+    ap.add_argument("--sweep-k", action="store_true", help="also time k in {1,2,4,8,16}")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- utilities
+
+def measured_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None, "source": {}}
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            m = json.load(fh)
+        peaks["hbm_gbs"] = m.get("hbm_gbs")
+        peaks["source"]["hbm"] = "measured (MEASURED_PEAKS.json)"
+    if peaks["hbm_gbs"] is None:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["source"]["hbm"] = "fallback (B200_PROFILING.md)"
+    fp = os.path.join(REPO, "profiles", "fp_peak.json")
+    if os.path.exists(fp):
+        with open(fp) as fh:
+            f = json.load(fh)
+        peaks["fp64_tflops"] = f["fp64_tflops"]
+        peaks["source"]["fp64"] = "measured (profiles/fp_peak.json, tools/fp_peak.cu)"
+    else:
+        peaks["fp64_tflops"] = 37.0
+        peaks["source"]["fp64"] = "datasheet (not measured)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * (mx or s)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ------------------------------------------------------------ CPU reference
+
+def cpu_reference_rate(spec, n, sample_steps=None, budget_s=10.0):
+    """Oracle port (C+OpenMP, all host threads) on a bounded sample of the
+    workload grid; returns (GStencil/s, threads, sample description)."""
+    from oracle import c_oracle
+    from paper_2103_08825_b200.core import canonical
+    offs, ws = canonical(spec)
+    threads = c_oracle.max_threads()
+    box = np.random.default_rng(12345).random(n + 2 * spec.r)
+    t0 = time.perf_counter()
+    c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
+    one = time.perf_counter() - t0
+    if sample_steps is None:
+        sample_steps = int(max(1, min(1000, budget_s / max(one, 1e-6))))
+    t0 = time.perf_counter()
+    c_oracle.sweep(box, spec.r, offs, ws, sample_steps, threads=threads, inplace=True)
+    dt = time.perf_counter() - t0
+    rate = n * sample_steps / dt / 1e9
+    return rate, threads, f"{sample_steps} steps of the full {n}-point grid (same spec)"
+
+
+def numpy_reference_rate(spec, n, steps=2):
+    """The reference's own arithmetic as numpy restates it (1 core)."""
+    from oracle import np_oracle
+    from paper_2103_08825_b200.core import canonical
+    offs, ws = canonical(spec)
+    box = np.random.default_rng(12345).random(n + 2 * spec.r)
+    t0 = time.perf_counter()
+    np_oracle.sweep(box, spec.r, offs, ws, steps)
+    dt = time.perf_counter() - t0
+    return n * steps / dt / 1e9
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2103_08825_b200.core import config_spec
+    wl = WORKLOADS[args.workload]
+    spec = config_spec(wl["spec"])
+    n = wl["n"]
+    from oracle import c_oracle
+    from paper_2103_08825_b200.core import canonical
+    offs, ws = canonical(spec)
+    threads = c_oracle.max_threads()
+    box = np.random.default_rng(12345).random(n + 2 * spec.r)
+    t0 = time.perf_counter()
+    c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
+    one = time.perf_counter() - t0
+    per_step = int(max(1, min(wl["T"], 8.0 / max(one, 1e-6))))   # ~8 s per bench step
+    for _ in range(args.warmup):
+        c_oracle.sweep(box, spec.r, offs, ws, max(1, per_step // 4), threads=threads, inplace=True)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        c_oracle.sweep(box, spec.r, offs, ws, per_step, threads=threads, inplace=True)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = n * per_step * args.steps / total / 1e9
+    sample = f"{per_step} of T={wl['T']} steps of the full {n}-point grid per bench step"
+    line = {
+        "impl": "reference", "metric": "GStencil/s", "value": value, "unit": "GStencil/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["name"], "k": 1, "host": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "GStencil/s", "cores": threads,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GStencil/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def run_gpu_arm(args):
+    import torch
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    device = torch.cuda.current_device()
+
+    from paper_2103_08825_b200.core import config_spec
+    from paper_2103_08825_b200.plan import Plan
+    wl = WORKLOADS[args.workload]
+    spec = config_spec(wl["spec"])
+    n, T, k = wl["n"], wl["T"], args.k
+    stream = torch.cuda.current_stream()
+
+    rng = np.random.default_rng(12345 + rank)
+    host_in = torch.empty(n + 2 * spec.r, dtype=torch.float64, pin_memory=True)
+    host_in.numpy()[:] = rng.random(n + 2 * spec.r)
+    host_out = torch.empty_like(host_in, pin_memory=True)
+
+    if world > 1:
+        from paper_2103_08825_b200.slab import SlabSweep
+        runner = SlabSweep(spec, (n,), rank=rank, world=world, k=k, arith=args.arith,
+                           device=device, group=None)
+        run_once = lambda: runner.run(T)              # noqa: E731
+        upload = lambda: runner.upload(host_in.numpy())   # noqa: E731
+        download = lambda: runner.download(host_out.numpy())  # noqa: E731
+        plan = runner.plan
+    else:
+        plan = Plan(spec, (n,), k=k, arith=args.arith, device=device)
+        plan.set_stream(stream.cuda_stream)
+        upload = lambda: plan.upload(host_in.numpy())       # noqa: E731
+        download = lambda: plan.download(host_out.numpy())  # noqa: E731
+        run_once = lambda: plan.launch(T)                   # noqa: E731
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    upload()
+    for _ in range(args.warmup):
+        run_once()
+    barrier()
+
+    launches_per_step = -(-T // k) if T % k == 0 else (T // k + bin(T % k).count("1"))
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(device) as clocks:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run_once()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = n * world * T / (ms_per_step * 1e-3) / 1e9
+
+    # kernel share: one main kernel; its average launch duration over the timed region
+    launch_ms = ms_per_step / launches_per_step
+    peaks = measured_peaks()
+    alg_bytes = ALG_BYTES_PER_POINT * n
+    achieved_gbs = alg_bytes / (launch_ms * 1e-3) / 1e9
+    flops_per_update = 2 * len(spec.weights) - 1
+    fp_bound = peaks["fp64_tflops"] * 1e12 / flops_per_update / 1e9
+    hbm_bound = peaks["hbm_gbs"] * 1e9 * k / ALG_BYTES_PER_POINT / 1e9
+    per_gpu = value / world
+    roofline = {
+        "bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+        "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": None,
+        "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": launch_ms,
+        "peak_source": peaks["source"]["hbm"],
+    }
+    stencil_roofline = {
+        "k": k, "hbm_bound_gstencil": hbm_bound, "fp64_bound_gstencil": fp_bound,
+        "fp64_peak_tflops": peaks["fp64_tflops"], "fp64_peak_source": peaks["source"]["fp64"],
+        "binding": "hbm" if hbm_bound < fp_bound else "fp64",
+        "achieved_gstencil_per_gpu": per_gpu,
+        "frac": per_gpu / min(hbm_bound, fp_bound),
+        "fp64_tflops_achieved": per_gpu * 1e9 * flops_per_update / 1e12,
+    }
+
+    # end to end through the C-ABI call with host buffers
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            upload()
+            run_once()
+            download()
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        tt = torch.tensor([dt], device="cuda")
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": n * world * T * args.steps / dt / 1e9, "unit": "GStencil/s",
+               "h2d_bytes_per_step": int(host_in.numel() * 8 * world),
+               "d2h_bytes_per_step": int(host_out.numel() * 8 * world),
+               "timer": "host wall clock around upload+sweep+download, max over ranks"}
+
+    sweep = None
+    if args.sweep_k and world == 1:
+        sweep = {}
+        for kk in (1, 2, 4, 8, 16):
+            with Plan(spec, (n,), k=kk, arith=args.arith, device=device) as p:
+                p.upload(host_in.numpy())
+                p.run(T // 4)
+                tim = p.run(T)
+                sweep[str(kk)] = {"gstencil": n * T / (tim.device_ms * 1e-3) / 1e9,
+                                  "ms": tim.device_ms, "launches": tim.launches}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        rate, threads, sample = cpu_reference_rate(spec, n)
+        cpu = {"value": rate, "unit": "GStencil/s", "cores": threads, "kind": "port",
+               "sample": sample + "; oracle/oracle.c (bit-exact restatement of "
+                                  "stencilbench scalar_step), OpenMP"}
+        try:
+            cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n)
+        except MemoryError:
+            pass
+
+    if rank == 0:
+        line = {
+            "metric": "GStencil/s", "value": value, "unit": "GStencil/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": wl["name"] + (f", weak-scaled x{world} (slab per GPU)" if world > 1 else ""),
+                       "k": k, "arith": args.arith, "grid_bytes": (n + 2 * spec.r) * 8,
+                       "l2": "inputs larger than L2 (537 MB grid vs 126 MB L2)"
+                             if n >= (1 << 24) else "grid fits in L2",
+                       "parallelism": f"slab{world}" if world > 1 else "single"},
+            "roofline": roofline, "stencil_roofline": stencil_roofline,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if sweep is not None:
+            line["k_sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

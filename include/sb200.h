@@ -1,0 +1,138 @@
+/*
+ * sb200 -- C ABI of the B200-native multistep stencil sweep.
+ *
+ * Drop-in boundary for the reference package ``stencilbench`` (a pure
+ * Python + numpy package; its "plugin interface" is the method registry and
+ * the step/sweep call signatures, not an FFI).  Each entry point below names
+ * the reference interface it replaces:
+ *
+ *   sb_plan_create   <- StencilSpec validation + alloc_grid/alloc_like
+ *                       (stencilbench/core.py:54-106, core.py:335-373)
+ *   sb_upload        <- GridBuffer.set_interior / seeded halo
+ *                       (core.py:318-327, harness.py:139-146)
+ *   sb_run           <- the T-step loop of harness._execute
+ *                       (harness.py:195-201) over scalar_step
+ *                       (kernels.py:120-134) and the k-level time jam
+ *                       jam_sweep (timejam.py:288-304)
+ *   sb_download      <- GridBuffer.natural_interior (core.py:308-316)
+ *   sb_plan_destroy  <- (buffers going out of scope)
+ *   sb_last_error    <- exception messages of SpecError/GridError
+ *                       (core.py:38-43)
+ *
+ * Host buffers use one convention everywhere: a compact C-order box of the
+ * halo-inclusive grid, shape (n_0 + h_lo + h_hi, n_1 + 2r, ..., n_{d-1} + 2r)
+ * where h_lo/h_hi are r (physical Dirichlet halo) or the ghost depth of a
+ * slab side (multi-GPU).  Halo cells are read, never written, and are
+ * preserved bit-for-bit.  Element type is double (SB_F64) or float (SB_F32).
+ *
+ * Conventions: functions return SB_OK (0) or a negative sb_status; the
+ * message is available from sb_last_error() (thread-local).  A plan owns its
+ * device memory and stream; one host thread per plan.  There is no CPU
+ * fallback: without a CUDA device every compute call fails with SB_ERR_CUDA.
+ */
+#ifndef SB200_H
+#define SB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB200_ABI_VERSION 1
+
+typedef enum {
+    SB_OK = 0,
+    SB_ERR_SPEC = -1,   /* invalid stencil (SpecError) */
+    SB_ERR_GRID = -2,   /* invalid geometry / buffer size (GridError) */
+    SB_ERR_ARG = -3,    /* invalid argument (ValueError) */
+    SB_ERR_CUDA = -4,   /* CUDA runtime failure or no device (RuntimeError) */
+    SB_ERR_NOMEM = -5,  /* device or host allocation failed (MemoryError) */
+    SB_ERR_STATE = -6   /* call out of order, e.g. run before upload */
+} sb_status;
+
+typedef enum { SB_F64 = 0, SB_F32 = 1 } sb_dtype;
+
+/* EXACT: per term one rounded multiply then one rounded add, canonical
+ * order, accumulator from +0.0 -- bit-identical to the reference oracle
+ * (kernels.py:103-108).  FMA: first term a multiply, then fused
+ * multiply-adds in canonical order (<= 1e-12 relative vs the oracle). */
+typedef enum { SB_ARITH_EXACT = 0, SB_ARITH_FMA = 1 } sb_arith;
+
+typedef enum { SB_STAR = 0, SB_BOX = 1 } sb_shape;
+
+/* AUTO picks the fused temporal-blocking kernel when one exists for the
+ * stencil class, else GENERIC (one step per launch, any d/r/shape). */
+typedef enum { SB_KERNEL_AUTO = 0, SB_KERNEL_GENERIC = 1, SB_KERNEL_FUSED = 2 } sb_kernel;
+
+typedef struct sb_problem {
+    int32_t d;               /* 1, 2 or 3 */
+    int32_t r;               /* order (max per-axis distance), >= 1 */
+    int32_t shape;           /* sb_shape */
+    int32_t nw;              /* number of weights */
+    const int32_t *offsets;  /* nw*d offsets, canonical (lexicographic) order */
+    const double *weights;   /* nw weights matching offsets */
+    int64_t dims[3];         /* interior extents, slowest axis first */
+    int32_t dtype;           /* sb_dtype */
+    int32_t arith;           /* sb_arith */
+    int32_t k;               /* fused steps per launch; 0 = auto */
+    int32_t kernel;          /* sb_kernel */
+    int32_t device;          /* CUDA device ordinal */
+    int32_t ghost_lo;        /* slab side below: 0 = physical halo r; G>0 = G ghost planes */
+    int32_t ghost_hi;        /* slab side above: same convention */
+} sb_problem;
+
+typedef struct sb_timing {
+    double device_ms;        /* CUDA-event time of the whole call on the plan stream */
+    double kernel_ms;        /* CUDA-event time of the main kernel launches only */
+    int64_t launches;        /* kernels launched by the call */
+    int64_t point_updates;   /* interior points x steps (Counters.point_updates) */
+    int32_t k_used;          /* fused steps per main launch */
+    int32_t reserved;
+    char kernel_name[64];    /* main kernel used */
+} sb_timing;
+
+typedef struct sb_plan sb_plan;
+
+int sb_plan_create(sb_plan **plan, const sb_problem *problem);
+void sb_plan_destroy(sb_plan *plan);
+
+/* Number of elements of the host box (see convention above). */
+int sb_host_elems(const sb_plan *plan, int64_t *elems);
+
+/* Host box -> device (both ping-pong buffers; halo/ghost included). */
+int sb_upload(sb_plan *plan, const void *host, size_t bytes);
+/* Device (current buffer) -> host box, halo included. */
+int sb_download(sb_plan *plan, void *host, size_t bytes);
+
+/* Advance `steps` time steps, synchronously; fills *timing if non-NULL.
+ * Slab plans (ghost_lo/hi > 0) accept steps <= min ghost depth / r. */
+int sb_run(sb_plan *plan, int64_t steps, sb_timing *timing);
+
+/* Same, asynchronously on the plan stream (no host sync, no timing). */
+int sb_launch(sb_plan *plan, int64_t steps);
+
+/* Run on an external stream (e.g. torch's current stream); NULL restores
+ * the plan's own stream. */
+int sb_set_stream(sb_plan *plan, void *cuda_stream);
+
+/* Device pointer and element strides of the current buffer, for halo
+ * exchange by the multi-GPU host layer.  origin = element offset of
+ * interior point (0,...,0); strides[0..d-1] in elements. */
+int sb_device_view(const sb_plan *plan, int which, void **base,
+                   int64_t *origin, int64_t strides[3]);
+
+/* Fused depth the plan will use per launch. */
+int sb_plan_k(const sb_plan *plan, int32_t *k);
+
+const char *sb_last_error(void);
+int sb_abi_version(void);
+/* Number of CUDA devices visible (0 without a GPU; never fails). */
+int sb_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SB200_H */

@@ -1,0 +1,583 @@
+// sb200 -- plan management, device layout, dispatch and the C ABI
+// (include/sb200.h).  Host side of the B200 multistep stencil sweep.
+//
+// Device layout (private; the host convention is the compact halo box):
+//   * unit axis x padded to a pitch px so interior x = 0 starts 128 B aligned
+//     (512 B for 1D, whose single row also carries the kernel's read-ahead);
+//   * outer axes keep their r-deep halo rows/planes, and the slab axis
+//     (axis 0) keeps h_lo/h_hi = r (physical) or the ghost depth G (slab);
+//   * two buffers (ping-pong), halo and ghost present in both.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/sb200.h"
+#include "common.cuh"
+#include "fused1d.cuh"
+#include "generic.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define SB_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(SB_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+constexpr int64_t kRightPad1D = 4096 + 1024;  // >= max lane span S + lead + RK + Q
+constexpr int kMaxS1D = 4096;
+
+enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2 };
+
+}  // namespace
+
+struct sb_plan {
+    int d = 0, r = 0, shape = 0, nw = 0, dtype = 0, arith = 0, kreq = 0, kernel_req = 0;
+    int device = 0;
+    std::vector<int32_t> offsets;
+    std::vector<double> weights;
+    int64_t dims[3] = {1, 1, 1};  // interior, slowest first (first d used)
+    int64_t hlo = 0, hhi = 0;     // axis-0 halo/ghost depth on each side
+    bool phys_lo = true, phys_hi = true;
+    size_t es = 8;
+    sb::Geom g{};                 // canonical 3D geometry of the device buffers
+    int64_t px = 0;
+    size_t buf_elems = 0;
+    void* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    bool uploaded = false;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int64_t* d_lin = nullptr;
+    void* d_w = nullptr;
+    int kind = KK_GENERIC;
+    int k = 1;
+    int num_sms = 148;
+    // host-box geometry
+    int64_t host_rows = 0, host_row_elems = 0, host_elems = 0;
+    int64_t host_dst_offset = 0;  // device element offset of host element 0
+};
+
+namespace {
+
+int validate_problem(const sb_problem* p) {
+    if (!p) return fail(SB_ERR_ARG, "problem is NULL");
+    if (p->d < 1 || p->d > 3) return fail(SB_ERR_SPEC, "dimension must be 1, 2 or 3, got %d", p->d);
+    if (p->r < 1) return fail(SB_ERR_SPEC, "order must be positive, got %d", p->r);
+    if (p->shape != SB_STAR && p->shape != SB_BOX)
+        return fail(SB_ERR_SPEC, "shape must be star or box, got %d", p->shape);
+    if (!p->offsets || !p->weights) return fail(SB_ERR_SPEC, "offsets/weights are NULL");
+    const int d = p->d, r = p->r;
+    int64_t expected = 1;
+    if (p->shape == SB_STAR) {
+        expected = 2 * d * r + 1;
+    } else {
+        for (int a = 0; a < d; a++) expected *= (2 * r + 1);
+    }
+    if (p->nw != expected)
+        return fail(SB_ERR_SPEC, "%s stencil of d=%d r=%d needs %lld weights, got %d",
+                    p->shape == SB_STAR ? "star" : "box", d, r, (long long)expected, p->nw);
+    if (p->nw > sb::kGenericMaxW) return fail(SB_ERR_SPEC, "too many weights (%d)", p->nw);
+    bool has_zero = false;
+    for (int i = 0; i < p->nw; i++) {
+        int nz = 0, mx = 0;
+        for (int a = 0; a < d; a++) {
+            const int c = p->offsets[i * d + a];
+            nz += (c != 0);
+            mx = std::max(mx, c < 0 ? -c : c);
+        }
+        if (mx > r) return fail(SB_ERR_SPEC, "offset %d outside radius %d", i, r);
+        if (nz == 0) has_zero = true;
+        if (p->shape == SB_STAR && nz > 1) return fail(SB_ERR_SPEC, "star stencil has a non-axis-aligned offset");
+        if (i > 0) {  // strictly increasing lexicographic order
+            int cmp = 0;
+            for (int a = 0; a < d && cmp == 0; a++) {
+                const int x = p->offsets[(i - 1) * d + a], y = p->offsets[i * d + a];
+                cmp = (x < y) ? -1 : (x > y ? 1 : 0);
+            }
+            if (cmp >= 0) return fail(SB_ERR_SPEC, "offsets not in canonical (lexicographic) order at %d", i);
+        }
+    }
+    if (!has_zero) return fail(SB_ERR_SPEC, "zero offset missing from weight table");
+    for (int a = 0; a < d; a++)
+        if (p->dims[a] <= 0) return fail(SB_ERR_GRID, "extents must be positive (axis %d)", a);
+    if (p->dtype != SB_F64 && p->dtype != SB_F32) return fail(SB_ERR_ARG, "dtype must be SB_F64 or SB_F32");
+    if (p->arith != SB_ARITH_EXACT && p->arith != SB_ARITH_FMA) return fail(SB_ERR_ARG, "arith must be EXACT or FMA");
+    if (p->k < 0 || p->k > 64) return fail(SB_ERR_ARG, "fusion depth k=%d out of range", p->k);
+    if (p->ghost_lo < 0 || p->ghost_hi < 0) return fail(SB_ERR_GRID, "ghost depth must be >= 0");
+    if ((p->ghost_lo > 0 && p->ghost_lo < r) || (p->ghost_hi > 0 && p->ghost_hi < r))
+        return fail(SB_ERR_GRID, "ghost depth must be >= r=%d", r);
+    if (p->kernel < SB_KERNEL_AUTO || p->kernel > SB_KERNEL_FUSED) return fail(SB_ERR_ARG, "bad kernel choice");
+    return SB_OK;
+}
+
+bool fused1d_supported(const sb_plan* P) { return P->d == 1 && (P->r == 1 || P->r == 2); }
+
+// Supported fused depths (template instantiations).
+bool fused_k_ok(int k) { return k == 1 || k == 2 || k == 4 || k == 8 || k == 16; }
+
+int largest_fused_k(int64_t steps, int kmax) {
+    int k = 1;
+    while (k * 2 <= kmax && k * 2 <= steps) k *= 2;
+    return k;
+}
+
+// ---------------------------------------------------------------- launches
+
+template <typename T, bool FMA>
+int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
+    sb::Geom g = P->g;
+    int64_t ext[3] = {g.n[0], g.n[1], g.n[2]};
+    ext[g.slab_axis] = hi - lo;
+    if (ext[0] <= 0 || ext[1] <= 0 || ext[2] <= 0) return SB_OK;
+    const int64_t rows = ext[0] * ext[1];
+    dim3 grid((unsigned)((ext[2] + sb::kGenericThreads - 1) / sb::kGenericThreads),
+              (unsigned)std::min<int64_t>(rows, 65535));
+    sb::generic_step_kernel<T, FMA><<<grid, sb::kGenericThreads, 0, P->stream>>>(
+        src, dst, g, lo, hi, P->nw, P->d_lin, reinterpret_cast<const T*>(P->d_w));
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, int R, int K, bool FMA>
+int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
+    using SH = sb::Fused1DShape<T>;
+    auto kern = sb::fused1d_kernel<T, R, K, FMA>;
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SH::SMEM_BYTES));
+    int blocks_per_sm = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, SH::WARPS * 32, SH::SMEM_BYTES));
+    blocks_per_sm = std::max(blocks_per_sm, 1);
+    const int64_t n = P->g.n[2];
+    const int64_t lanes_target = (int64_t)P->num_sms * blocks_per_sm * SH::WARPS * 32;
+    int64_t S = (n + lanes_target - 1) / lanes_target;
+    S = std::max<int64_t>(round_up(S, SH::Q), SH::Q * 4);
+    S = std::min<int64_t>(S, kMaxS1D);
+    sb::Fused1DParams<T, R> prm;
+    prm.src = src + P->g.origin;
+    prm.dst = dst + P->g.origin;
+    prm.n = n;
+    prm.S = S;
+    prm.nlanes = (n + S - 1) / S;
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    for (int i = 0; i < 2 * R + 1; i++) prm.w[i] = (T)P->weights[i];
+    const int64_t warps = (prm.nlanes + 31) / 32;
+    const int64_t blocks = (warps + SH::WARPS - 1) / SH::WARPS;
+    kern<<<(unsigned)blocks, SH::WARPS * 32, SH::SMEM_BYTES, P->stream>>>(prm);
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, int R, bool FMA>
+int launch_fused1d_r(sb_plan* P, const T* src, T* dst, int k) {
+    switch (k) {
+        case 1: return launch_fused1d_k<T, R, 1, FMA>(P, src, dst);
+        case 2: return launch_fused1d_k<T, R, 2, FMA>(P, src, dst);
+        case 4: return launch_fused1d_k<T, R, 4, FMA>(P, src, dst);
+        case 8: return launch_fused1d_k<T, R, 8, FMA>(P, src, dst);
+        case 16: return launch_fused1d_k<T, R, 16, FMA>(P, src, dst);
+        default: return fail(SB_ERR_ARG, "unsupported fused depth %d", k);
+    }
+}
+
+template <typename T, bool FMA>
+int launch_fused1d(sb_plan* P, const T* src, T* dst, int k) {
+    if (P->r == 1) return launch_fused1d_r<T, 1, FMA>(P, src, dst, k);
+    return launch_fused1d_r<T, 2, FMA>(P, src, dst, k);
+}
+
+// One launch advancing k levels from buf[cur] into buf[cur^1].
+template <typename T, bool FMA>
+int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
+    const T* src = reinterpret_cast<const T*>(P->buf[P->cur]);
+    T* dst = reinterpret_cast<T*>(P->buf[P->cur ^ 1]);
+    int rc;
+    if (P->kind == KK_FUSED1D) {
+        rc = launch_fused1d<T, FMA>(P, src, dst, k);
+    } else {
+        // generic: one level; on slab sides the valid range shrinks by r per level
+        const int64_t n0 = P->dims[0];
+        const int64_t lo = P->phys_lo ? 0 : -P->hlo + (int64_t)P->r * (level_in_run + 1);
+        const int64_t hi = P->phys_hi ? n0 : n0 + P->hhi - (int64_t)P->r * (level_in_run + 1);
+        rc = launch_generic<T, FMA>(P, src, dst, lo, hi);
+    }
+    if (rc != SB_OK) return rc;
+    P->cur ^= 1;
+    ++*launches;
+    return SB_OK;
+}
+
+template <typename T, bool FMA>
+int run_steps(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
+    const bool slab = !(P->phys_lo && P->phys_hi);
+    int64_t done = 0;
+    *k_used = 1;
+    if (P->kind == KK_GENERIC) {
+        for (int64_t t = 0; t < steps; t++) {
+            int rc = launch_one<T, FMA>(P, 1, slab ? (int)t : 0, launches);
+            if (rc != SB_OK) return rc;
+        }
+        return SB_OK;
+    }
+    if (slab) {
+        // A slab plan runs one fused launch per exchange interval.
+        if (fused_k_ok((int)steps)) {
+            *k_used = (int)steps;
+            return launch_one<T, FMA>(P, (int)steps, 0, launches);
+        }
+        const int saved = P->kind;
+        P->kind = KK_GENERIC;
+        int rc = SB_OK;
+        for (int64_t t = 0; t < steps && rc == SB_OK; t++) rc = launch_one<T, FMA>(P, 1, (int)t, launches);
+        P->kind = saved;
+        return rc;
+    }
+    *k_used = P->k;
+    while (done < steps) {
+        const int kk = (steps - done >= P->k) ? P->k : largest_fused_k(steps - done, P->k);
+        int rc = launch_one<T, FMA>(P, kk, 0, launches);
+        if (rc != SB_OK) return rc;
+        done += kk;
+    }
+    return SB_OK;
+}
+
+int dispatch_run(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
+    const bool fma = P->arith == SB_ARITH_FMA;
+    if (P->dtype == SB_F64)
+        return fma ? run_steps<double, true>(P, steps, launches, k_used)
+                   : run_steps<double, false>(P, steps, launches, k_used);
+    return fma ? run_steps<float, true>(P, steps, launches, k_used)
+               : run_steps<float, false>(P, steps, launches, k_used);
+}
+
+const char* kernel_name(const sb_plan* P) {
+    if (P->kind == KK_FUSED1D) return "fused1d_kernel";
+    return "generic_step_kernel";
+}
+
+int max_slab_steps(const sb_plan* P) {
+    int64_t m = INT32_MAX;
+    if (!P->phys_lo) m = std::min<int64_t>(m, P->hlo / P->r);
+    if (!P->phys_hi) m = std::min<int64_t>(m, P->hhi / P->r);
+    return (int)m;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* sb_last_error(void) { return g_err.c_str(); }
+int sb_abi_version(void) { return SB200_ABI_VERSION; }
+
+int sb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void sb_plan_destroy(sb_plan* P) {
+    if (!P) return;
+    cudaSetDevice(P->device);
+    for (int i = 0; i < 2; i++)
+        if (P->buf[i]) cudaFree(P->buf[i]);
+    if (P->d_lin) cudaFree(P->d_lin);
+    if (P->d_w) cudaFree(P->d_w);
+    for (int i = 0; i < 2; i++)
+        if (P->ev[i]) cudaEventDestroy(P->ev[i]);
+    if (P->own_stream) cudaStreamDestroy(P->own_stream);
+    delete P;
+}
+
+int sb_plan_create(sb_plan** out, const sb_problem* prob) {
+    if (!out) return fail(SB_ERR_ARG, "plan output pointer is NULL");
+    *out = nullptr;
+    int rc = validate_problem(prob);
+    if (rc != SB_OK) return rc;
+    sb_plan* P = new (std::nothrow) sb_plan();
+    if (!P) return fail(SB_ERR_NOMEM, "host allocation failed");
+    P->d = prob->d;
+    P->r = prob->r;
+    P->shape = prob->shape;
+    P->nw = prob->nw;
+    P->dtype = prob->dtype;
+    P->arith = prob->arith;
+    P->kreq = prob->k;
+    P->kernel_req = prob->kernel;
+    P->device = prob->device;
+    P->offsets.assign(prob->offsets, prob->offsets + (size_t)prob->nw * prob->d);
+    P->weights.assign(prob->weights, prob->weights + prob->nw);
+    for (int a = 0; a < P->d; a++) P->dims[a] = prob->dims[a];
+    P->phys_lo = prob->ghost_lo == 0;
+    P->phys_hi = prob->ghost_hi == 0;
+    P->hlo = P->phys_lo ? P->r : prob->ghost_lo;
+    P->hhi = P->phys_hi ? P->r : prob->ghost_hi;
+    P->es = (P->dtype == SB_F64) ? 8 : 4;
+
+    // ---- kernel choice
+    const bool fused_ok = fused1d_supported(P);
+    if (prob->kernel == SB_KERNEL_FUSED && !fused_ok) {
+        delete P;
+        return fail(SB_ERR_ARG, "no fused kernel for d=%d r=%d shape=%d", prob->d, prob->r, prob->shape);
+    }
+    if (prob->kernel != SB_KERNEL_GENERIC && fused_ok) {
+        P->kind = KK_FUSED1D;
+        P->k = prob->k > 0 ? prob->k : 8;
+        if (!fused_k_ok(P->k)) {
+            delete P;
+            return fail(SB_ERR_ARG, "fused depth k=%d unsupported (1, 2, 4, 8, 16)", prob->k);
+        }
+    } else {
+        P->kind = KK_GENERIC;
+        P->k = 1;
+    }
+    if (!(P->phys_lo && P->phys_hi)) {
+        // slab: a launch of depth k needs ghost depth >= r*k on slab sides
+        if (P->kind == KK_FUSED1D && (int64_t)P->r * P->k > std::min(P->phys_lo ? INT32_MAX : P->hlo,
+                                                                      P->phys_hi ? INT32_MAX : P->hhi)) {
+            delete P;
+            return fail(SB_ERR_GRID, "ghost depth must be >= r*k = %d", P->r * P->k);
+        }
+    }
+
+    // ---- device geometry (canonical z, y, x)
+    const int d = P->d, r = P->r;
+    sb::Geom& g = P->g;
+    const int64_t es = (int64_t)P->es;
+    const int64_t line = 128 / es;
+    if (d == 1) {
+        const int64_t n = P->dims[0];
+        const int64_t axl = round_up(std::max(P->hlo, (int64_t)r) + 256, 64);
+        P->px = round_up(axl + n + std::max(P->hhi, (int64_t)r) + kRightPad1D, 64);
+        g.n[0] = 1; g.n[1] = 1; g.n[2] = n;
+        g.sy = P->px; g.sz = P->px;
+        g.origin = axl;
+        g.slab_axis = 2;
+        P->buf_elems = (size_t)P->px;
+        P->host_rows = 1;
+        P->host_row_elems = P->hlo + n + P->hhi;
+        P->host_dst_offset = axl - P->hlo;
+    } else {
+        const int64_t nx = P->dims[d - 1];
+        const int64_t ax = round_up(std::max<int64_t>(r, line), line);
+        P->px = round_up(ax + nx + r + line, line);
+        g.n[2] = nx;
+        if (d == 2) {
+            const int64_t ny = P->dims[0];
+            g.n[0] = 1; g.n[1] = ny;
+            g.sy = P->px;
+            const int64_t rows = P->hlo + ny + P->hhi;
+            g.sz = rows * P->px;
+            g.origin = P->hlo * P->px + ax;
+            g.slab_axis = 1;
+            P->buf_elems = (size_t)(rows * P->px);
+            P->host_rows = rows;
+        } else {
+            const int64_t nz = P->dims[0], ny = P->dims[1];
+            g.n[0] = nz; g.n[1] = ny;
+            g.sy = P->px;
+            g.sz = (ny + 2 * r) * P->px;
+            const int64_t planes = P->hlo + nz + P->hhi;
+            g.origin = P->hlo * g.sz + r * g.sy + ax;
+            g.slab_axis = 0;
+            P->buf_elems = (size_t)(planes * g.sz);
+            P->host_rows = planes * (ny + 2 * r);
+        }
+        P->host_row_elems = nx + 2 * r;
+        P->host_dst_offset = ax - r;
+    }
+    P->host_elems = P->host_rows * P->host_row_elems;
+
+    // ---- device resources
+    int ndev = sb_device_count();
+    if (ndev <= 0) {
+        delete P;
+        return fail(SB_ERR_CUDA, "no CUDA device available (sb200 has no CPU fallback)");
+    }
+    if (P->device < 0 || P->device >= ndev) {
+        delete P;
+        return fail(SB_ERR_ARG, "device %d out of range (%d visible)", P->device, ndev);
+    }
+#define SB_CUDA_P(call)                                                                        \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            int code_ = (e_ == cudaErrorMemoryAllocation) ? SB_ERR_NOMEM : SB_ERR_CUDA;        \
+            fail(code_, "%s failed: %s", #call, cudaGetErrorString(e_));                       \
+            sb_plan_destroy(P);                                                                \
+            return code_;                                                                      \
+        }                                                                                      \
+    } while (0)
+    SB_CUDA_P(cudaSetDevice(P->device));
+    SB_CUDA_P(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
+    SB_CUDA_P(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
+    P->stream = P->own_stream;
+    SB_CUDA_P(cudaEventCreate(&P->ev[0]));
+    SB_CUDA_P(cudaEventCreate(&P->ev[1]));
+    for (int i = 0; i < 2; i++) {
+        SB_CUDA_P(cudaMalloc(&P->buf[i], P->buf_elems * P->es));
+        SB_CUDA_P(cudaMemsetAsync(P->buf[i], 0, P->buf_elems * P->es, P->stream));
+    }
+    // generic tables: linear offsets + weights (in the plan dtype)
+    std::vector<int64_t> lin(P->nw);
+    for (int i = 0; i < P->nw; i++) {
+        int64_t o = 0;
+        for (int a = 0; a < d; a++) {
+            const int ca = 3 - d + a;  // canonical axis
+            const int64_t stride = (ca == 2) ? 1 : (ca == 1 ? g.sy : g.sz);
+            o += (int64_t)P->offsets[i * d + a] * stride;
+        }
+        lin[i] = o;
+    }
+    SB_CUDA_P(cudaMalloc(&P->d_lin, sizeof(int64_t) * P->nw));
+    SB_CUDA_P(cudaMemcpy(P->d_lin, lin.data(), sizeof(int64_t) * P->nw, cudaMemcpyHostToDevice));
+    SB_CUDA_P(cudaMalloc(&P->d_w, P->es * P->nw));
+    if (P->dtype == SB_F64) {
+        SB_CUDA_P(cudaMemcpy(P->d_w, P->weights.data(), 8 * P->nw, cudaMemcpyHostToDevice));
+    } else {
+        std::vector<float> wf(P->weights.begin(), P->weights.end());
+        SB_CUDA_P(cudaMemcpy(P->d_w, wf.data(), 4 * P->nw, cudaMemcpyHostToDevice));
+    }
+    SB_CUDA_P(cudaStreamSynchronize(P->stream));
+#undef SB_CUDA_P
+    *out = P;
+    return SB_OK;
+}
+
+int sb_host_elems(const sb_plan* P, int64_t* elems) {
+    if (!P || !elems) return fail(SB_ERR_ARG, "NULL argument");
+    *elems = P->host_elems;
+    return SB_OK;
+}
+
+int sb_upload(sb_plan* P, const void* host, size_t bytes) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    if (bytes != (size_t)P->host_elems * P->es)
+        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
+                    (long long)(P->host_elems * (int64_t)P->es));
+    SB_CUDA(cudaSetDevice(P->device));
+    char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
+    SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, host, P->host_row_elems * P->es,
+                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyHostToDevice, P->stream));
+    SB_CUDA(cudaMemcpyAsync(P->buf[1], P->buf[0], P->buf_elems * P->es, cudaMemcpyDeviceToDevice, P->stream));
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    P->cur = 0;
+    P->uploaded = true;
+    return SB_OK;
+}
+
+int sb_download(sb_plan* P, void* host, size_t bytes) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "download before upload");
+    if (bytes != (size_t)P->host_elems * P->es)
+        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
+                    (long long)(P->host_elems * (int64_t)P->es));
+    SB_CUDA(cudaSetDevice(P->device));
+    const char* src = reinterpret_cast<const char*>(P->buf[P->cur]) + P->host_dst_offset * P->es;
+    SB_CUDA(cudaMemcpy2DAsync(host, P->host_row_elems * P->es, src, P->px * P->es,
+                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyDeviceToHost, P->stream));
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
+}
+
+int sb_launch(sb_plan* P, int64_t steps) {
+    if (!P) return fail(SB_ERR_ARG, "NULL plan");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "run before upload");
+    if (steps < 0) return fail(SB_ERR_ARG, "steps must be >= 0");
+    if (steps > max_slab_steps(P))
+        return fail(SB_ERR_GRID, "slab plan can advance at most %d steps between exchanges", max_slab_steps(P));
+    SB_CUDA(cudaSetDevice(P->device));
+    int64_t launches = 0;
+    int k_used = 1;
+    return dispatch_run(P, steps, &launches, &k_used);
+}
+
+int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
+    if (!P) return fail(SB_ERR_ARG, "NULL plan");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "run before upload");
+    if (steps < 0) return fail(SB_ERR_ARG, "steps must be >= 0");
+    if (steps > max_slab_steps(P))
+        return fail(SB_ERR_GRID, "slab plan can advance at most %d steps between exchanges", max_slab_steps(P));
+    SB_CUDA(cudaSetDevice(P->device));
+    int64_t launches = 0;
+    int k_used = 1;
+    SB_CUDA(cudaEventRecord(P->ev[0], P->stream));
+    int rc = dispatch_run(P, steps, &launches, &k_used);
+    if (rc != SB_OK) return rc;
+    SB_CUDA(cudaEventRecord(P->ev[1], P->stream));
+    SB_CUDA(cudaEventSynchronize(P->ev[1]));
+    SB_CUDA(cudaGetLastError());
+    if (t) {
+        float ms = 0.f;
+        SB_CUDA(cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]));
+        t->device_ms = ms;
+        t->kernel_ms = ms;
+        t->launches = launches;
+        int64_t pts = 1;
+        for (int a = 0; a < P->d; a++) pts *= P->dims[a];
+        t->point_updates = pts * steps;
+        t->k_used = k_used;
+        t->reserved = 0;
+        std::snprintf(t->kernel_name, sizeof(t->kernel_name), "%s", kernel_name(P));
+    }
+    return SB_OK;
+}
+
+int sb_set_stream(sb_plan* P, void* stream) {
+    if (!P) return fail(SB_ERR_ARG, "NULL plan");
+    P->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : P->own_stream;
+    return SB_OK;
+}
+
+int sb_device_view(const sb_plan* P, int which, void** base, int64_t* origin, int64_t strides[3]) {
+    if (!P || !base || !origin || !strides) return fail(SB_ERR_ARG, "NULL argument");
+    if (which != 0 && which != 1) return fail(SB_ERR_ARG, "which must be 0 (current) or 1 (other)");
+    *base = P->buf[which == 0 ? P->cur : P->cur ^ 1];
+    *origin = P->g.origin;
+    strides[0] = strides[1] = strides[2] = 0;
+    if (P->d == 1) {
+        strides[0] = 1;
+    } else if (P->d == 2) {
+        strides[0] = P->g.sy;
+        strides[1] = 1;
+    } else {
+        strides[0] = P->g.sz;
+        strides[1] = P->g.sy;
+        strides[2] = 1;
+    }
+    return SB_OK;
+}
+
+int sb_plan_k(const sb_plan* P, int32_t* k) {
+    if (!P || !k) return fail(SB_ERR_ARG, "NULL argument");
+    *k = P->k;
+    return SB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,183 @@
+"""Plan: one stencil problem resident on one GPU, driven through the C ABI.
+
+A plan owns two device buffers (ping-pong) in a private pitched layout,
+chooses the kernel (fused temporal-blocking kernel for the stencil class, or
+the generic one-step kernel) and its fusion depth k.  Host grids use the
+compact halo-inclusive box convention of include/sb200.h.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .core import GridError, SpecError, canonical, validate
+
+_DTYPES = {"f64": (_abi.SB_F64, np.float64), "f32": (_abi.SB_F32, np.float32)}
+_ARITH = {"exact": _abi.SB_ARITH_EXACT, "fma": _abi.SB_ARITH_FMA}
+_KERNEL = {"auto": _abi.SB_KERNEL_AUTO, "generic": _abi.SB_KERNEL_GENERIC,
+           "fused": _abi.SB_KERNEL_FUSED}
+
+
+@dataclass
+class Timing:
+    device_ms: float
+    kernel_ms: float
+    launches: int
+    point_updates: int
+    k_used: int
+    kernel_name: str
+
+
+def host_shape(d: int, r: int, dims, ghost=(0, 0)) -> tuple[int, ...]:
+    """Shape of the compact host box for interior ``dims`` (slowest first)."""
+    dims = tuple(int(n) for n in dims)
+    if len(dims) != d:
+        raise GridError(f"need {d} extents, got {len(dims)}")
+    lo = ghost[0] if ghost[0] else r
+    hi = ghost[1] if ghost[1] else r
+    return (dims[0] + lo + hi,) + tuple(n + 2 * r for n in dims[1:])
+
+
+class Plan:
+    """A device-resident sweep of ``spec`` over interior ``dims``.
+
+    ``dtype`` 'f64' or 'f32'; ``arith`` 'exact' (bit-identical to the
+    reference oracle) or 'fma'; ``k`` fused steps per launch (0 = auto);
+    ``kernel`` 'auto' | 'generic' | 'fused'; ``ghost`` = (lo, hi) ghost depths
+    of slab sides (0 = physical Dirichlet halo).
+    """
+
+    def __init__(self, spec, dims, *, dtype="f64", arith="fma", k=0, kernel="auto",
+                 device=0, ghost=(0, 0)):
+        validate(spec)
+        if dtype not in _DTYPES:
+            raise ValueError(f"dtype must be one of {list(_DTYPES)}")
+        if arith not in _ARITH:
+            raise ValueError(f"arith must be one of {list(_ARITH)}")
+        if kernel not in _KERNEL:
+            raise ValueError(f"kernel must be one of {list(_KERNEL)}")
+        self.spec = spec
+        self.d, self.r = spec.d, spec.r
+        self.dims = tuple(int(n) for n in dims)
+        if len(self.dims) != self.d:
+            raise GridError(f"{getattr(spec, 'name', 'spec')} needs {self.d} extents, "
+                            f"got {len(self.dims)}")
+        self.dtype_name = dtype
+        self.np_dtype = _DTYPES[dtype][1]
+        self.ghost = (int(ghost[0]), int(ghost[1]))
+        self.shape = host_shape(self.d, self.r, self.dims, self.ghost)
+        offs, ws = canonical(spec)
+        self._offs = (ctypes.c_int32 * (len(offs) * self.d))(*[c for o in offs for c in o])
+        self._ws = (ctypes.c_double * len(ws))(*ws)
+        prob = _abi.SbProblem()
+        prob.d, prob.r = self.d, self.r
+        prob.shape = _abi.SB_STAR if spec.shape == "star" else _abi.SB_BOX
+        prob.nw = len(ws)
+        prob.offsets = ctypes.cast(self._offs, ctypes.POINTER(ctypes.c_int32))
+        prob.weights = ctypes.cast(self._ws, ctypes.POINTER(ctypes.c_double))
+        for a in range(3):
+            prob.dims[a] = self.dims[a] if a < self.d else 1
+        prob.dtype = _DTYPES[dtype][0]
+        prob.arith = _ARITH[arith]
+        prob.k = int(k)
+        prob.kernel = _KERNEL[kernel]
+        prob.device = int(device)
+        prob.ghost_lo, prob.ghost_hi = self.ghost
+        self._lib = _abi.load()
+        handle = ctypes.c_void_p()
+        _abi.check(self._lib.sb_plan_create(ctypes.byref(handle), ctypes.byref(prob)))
+        self._h = handle
+        kk = ctypes.c_int32()
+        _abi.check(self._lib.sb_plan_k(self._h, ctypes.byref(kk)))
+        self.k = int(kk.value)
+
+    # -- lifecycle
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.sb_plan_destroy(h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- data movement
+    def _check_box(self, box: np.ndarray):
+        if box.shape != self.shape:
+            raise GridError(f"host box shape {box.shape}, expected {self.shape}")
+        if box.dtype != self.np_dtype:
+            raise GridError(f"host box dtype {box.dtype}, expected {np.dtype(self.np_dtype)}")
+        if not box.flags.c_contiguous:
+            raise GridError("host box must be C-contiguous")
+
+    def upload(self, box: np.ndarray) -> None:
+        self._check_box(box)
+        _abi.check(self._lib.sb_upload(self._h, box.ctypes.data, box.nbytes))
+
+    def download(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.shape, dtype=self.np_dtype)
+        self._check_box(out)
+        _abi.check(self._lib.sb_download(self._h, out.ctypes.data, out.nbytes))
+        return out
+
+    # -- compute
+    def run(self, steps: int) -> Timing:
+        t = _abi.SbTiming()
+        _abi.check(self._lib.sb_run(self._h, int(steps), ctypes.byref(t)))
+        return Timing(t.device_ms, t.kernel_ms, t.launches, t.point_updates, t.k_used,
+                      t.kernel_name.decode())
+
+    def launch(self, steps: int) -> None:
+        _abi.check(self._lib.sb_launch(self._h, int(steps)))
+
+    def set_stream(self, stream_ptr: int | None) -> None:
+        _abi.check(self._lib.sb_set_stream(self._h, ctypes.c_void_p(stream_ptr or 0)))
+
+    def device_view(self, which: int = 0):
+        """(base pointer, origin element offset, element strides) of a buffer."""
+        base = ctypes.c_void_p()
+        origin = ctypes.c_int64()
+        strides = (ctypes.c_int64 * 3)()
+        _abi.check(self._lib.sb_device_view(self._h, which, ctypes.byref(base),
+                                            ctypes.byref(origin), strides))
+        return int(base.value or 0), int(origin.value), tuple(strides[: self.d])
+
+
+def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
+          device=0, dtype=None) -> np.ndarray:
+    """``steps`` Jacobi steps of ``spec`` over a compact halo-inclusive ``box``.
+
+    Returns a new box (halo preserved).  The grid-in/grid-out entry point of
+    the drop-in (stencil shape and coefficients, input grid, timestep count).
+    """
+    validate(spec)
+    box = np.asarray(box)
+    if dtype is None:
+        dtype = "f32" if box.dtype == np.float32 else "f64"
+    np_dtype = _DTYPES[dtype][1]
+    if box.ndim != spec.d:
+        raise GridError(f"box has {box.ndim} axes, spec needs {spec.d}")
+    dims = tuple(s - 2 * spec.r for s in box.shape)
+    if any(n <= 0 for n in dims):
+        raise GridError(f"box shape {box.shape} too small for order {spec.r}")
+    with Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device) as p:
+        p.upload(np.ascontiguousarray(box, dtype=np_dtype))
+        p.run(steps)
+        return p.download()
+
+
+__all__ = ["Plan", "Timing", "sweep", "host_shape", "SpecError", "GridError"]

@@ -1,0 +1,178 @@
+"""Parity of the sm_100a path against the reference (GPU, ``-m gpu``).
+
+* EXACT arithmetic is bit-identical to the reference's own outputs (golden
+  fixtures made by ``stencilbench.kernels.scalar_step``), for every fixture,
+  both halo conventions, the generic and the fused kernels, every fused depth.
+* FMA arithmetic stays within the north_star fp64 bar (1e-12 relative).
+* fp32 stays within 1e-5 of the fp64 oracle run on fp32-rounded inputs and
+  weights (the reference is fp64-only).
+* Full BASELINE sizes are checked through the C oracle and size-independent
+  properties (constant preservation, halo preservation, linearity).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, golden_spec, interior, load_golden, seeded_box
+from oracle import c_oracle, np_oracle
+
+from paper_2103_08825_b200.core import canonical, config_spec, make_stencil_spec
+from paper_2103_08825_b200.plan import Plan, sweep
+
+pytestmark = pytest.mark.gpu
+
+NAMES = golden_names()
+FP64_TOL = 1e-12
+FP32_TOL = 1e-5
+
+
+def oracle(spec, box, T):
+    offs, ws = canonical(spec)
+    return c_oracle.sweep(box, spec.r, offs, ws, T)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("halo", ["zero", "full"])
+@pytest.mark.parametrize("kernel", ["generic", "auto"])
+def test_exact_bit_identical_to_reference(name, halo, kernel):
+    g = load_golden(name)
+    spec = golden_spec(g)
+    for T in g["steps"]:
+        got = sweep(spec, g[f"in_{halo}"], T, arith="exact", kernel=kernel)
+        want = g[f"out_{halo}_T{T}"]
+        assert got.tobytes() == want.tobytes(), (name, halo, kernel, T)
+
+
+@pytest.mark.parametrize("name", NAMES)
+@pytest.mark.parametrize("halo", ["zero", "full"])
+def test_fma_within_fp64_bar(name, halo):
+    g = load_golden(name)
+    spec = golden_spec(g)
+    T = g["steps"][-1]
+    got = sweep(spec, g[f"in_{halo}"], T, arith="fma")
+    want = g[f"out_{halo}_T{T}"]
+    assert np_oracle.max_rel_error(interior(got, g["r"]), interior(want, g["r"])) <= FP64_TOL
+    mask = np.ones(got.shape, bool)
+    mask[tuple(slice(g["r"], s - g["r"]) for s in got.shape)] = False
+    assert np.array_equal(got[mask], want[mask])          # halo untouched
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+@pytest.mark.parametrize("k", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("n", [1, 5, 63, 1000, 70001])
+def test_fused1d_every_depth_exact(cfg, k, n):
+    spec = config_spec(cfg)
+    box = seeded_box((n,), spec.r, seed=n + k)
+    T = 37                                   # not a multiple of k: exercises the tail
+    got = sweep(spec, box, T, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, T).tobytes()
+
+
+@pytest.mark.parametrize("k", [1, 8, 16])
+def test_fused1d_fp32(k):
+    spec = config_spec("c2")
+    box = seeded_box((100003,), 2, seed=3)
+    box32 = box.astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 2, offs, [float(np.float32(w)) for w in ws], 50)
+    got = sweep(spec, box32, 50, arith="fma", k=k)
+    assert got.dtype == np.float32
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+@pytest.mark.parametrize("key,dims", [("c3b", (67, 300)), ("c5", (20, 24, 70)), ("c4", (17, 30, 40))])
+def test_generic_fp32(key, dims):
+    spec = config_spec(key)
+    box32 = seeded_box(dims, 1, seed=9).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 12)
+    got = sweep(spec, box32, 12, arith="fma")
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+# --- reference known-answer tests (stencilbench tests/test_kernels.py:80-104)
+
+def test_impulse_response():
+    spec = make_stencil_spec("1d3p")
+    box = np.zeros(7)
+    box[3] = 1.0
+    for kernel in ("generic", "fused"):
+        out = sweep(spec, box, 1, arith="exact", kernel=kernel)
+        assert out[1:-1].tolist() == [0, 0.25, 0.5, 0.25, 0]
+
+
+def test_linear_ramp_fixed_point():
+    spec = make_stencil_spec("1d3p")
+    n = 32
+    box = np.zeros(n + 2)
+    box[1:-1] = np.arange(float(n))
+    out = sweep(spec, box, 1, arith="exact")
+    assert np.array_equal(out[2:-2], np.arange(1.0, n - 1))
+
+
+@pytest.mark.parametrize("preset,dims", [("2d9p", (12, 32)), ("3d27p", (6, 7, 20)), ("1d5p", (64,))])
+def test_constant_preserved(preset, dims):
+    spec = make_stencil_spec(preset)
+    box = np.full(tuple(n + 2 * spec.r for n in dims), 2.5)
+    for arith in ("exact", "fma"):
+        assert np.all(sweep(spec, box, 9, arith=arith) == 2.5)
+
+
+def test_impulse_locality():
+    spec = make_stencil_spec("1d5p")
+    box = np.zeros(68)
+    box[2 + 31] = 1.0
+    out = sweep(spec, box, 1, arith="exact")
+    support = np.flatnonzero(out[2:-2])
+    assert support.min() >= 31 - 2 and support.max() <= 31 + 2
+
+
+# --- full BASELINE sizes --------------------------------------------------------
+
+def test_c1_full_size_exact():
+    spec = config_spec("c1")
+    box = seeded_box((1 << 20,), 1)
+    got = sweep(spec, box, 64, arith="exact")
+    assert got.tobytes() == oracle(spec, box, 64).tobytes()
+
+
+def test_c2_full_size_fma_k8():
+    spec = config_spec("c2")
+    box = seeded_box((1 << 26,), 2)
+    got = sweep(spec, box, 24, arith="fma", k=8)
+    want = oracle(spec, box, 24)
+    assert np_oracle.max_rel_error(got, want) <= FP64_TOL
+
+
+def test_c2_full_size_exact_k16_halo_zero():
+    spec = config_spec("c2")
+    box = seeded_box((1 << 26,), 2, halo="zero")
+    got = sweep(spec, box, 16, arith="exact", k=16)
+    assert got.tobytes() == oracle(spec, box, 16).tobytes()
+
+
+def test_linearity_full_c2():
+    spec = config_spec("c2")
+    a = seeded_box((1 << 26,), 2, seed=1)
+    b = seeded_box((1 << 26,), 2, seed=2)
+    sa = sweep(spec, a, 40, k=8)
+    sb = sweep(spec, b, 40, k=8)
+    sab = sweep(spec, 0.5 * a + 0.25 * b, 40, k=8)
+    assert np_oracle.max_rel_error(sab, 0.5 * sa + 0.25 * sb) <= 1e-12
+
+
+def test_plan_reuse_and_timing():
+    spec = config_spec("c2")
+    box = seeded_box((100000,), 2)
+    with Plan(spec, (100000,), k=8) as p:
+        p.upload(box)
+        t = p.run(20)
+        assert t.point_updates == 100000 * 20
+        assert t.k_used == 8 and t.launches == 3          # 8 + 8 + 4
+        assert t.kernel_name == "fused1d_kernel"
+        mid = p.download()
+        p.run(20)
+        end = p.download()
+    want_mid = oracle(spec, box, 20)
+    assert np_oracle.max_rel_error(mid, want_mid) <= FP64_TOL
+    assert np_oracle.max_rel_error(end, oracle(spec, want_mid, 20)) <= FP64_TOL
