@@ -3,7 +3,7 @@
 
 Workload (N=1): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
 N=2^26 interior points, T=1000 steps, coefficients (1/16, 1/4, 3/8, 1/4,
-1/16), fixed halo, fusion depth k swept over {1,2,4,8} (default k=8).
+1/16), fixed halo, fusion depth k swept over {1,2,4,8,16} (default k=16, the fastest).
 One bench "step" = one full sweep (T=1000 time steps over the whole grid).
 At N>1 GPUs the same workload is weak-scaled: each rank owns a 2^26-point
 slab of a 2^26*N-point line, with an r*k-deep ghost exchange every launch.
@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
-    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--k", type=int, default=16)
     ap.add_argument("--arith", default="fma", choices=["fma", "exact"])
     ap.add_argument("--sweep-k", action="store_true", help="also time k in {1,2,4,8,16}")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -239,7 +239,10 @@ def run_gpu_arm(args):
     wl = WORKLOADS[args.workload]
     spec = config_spec(wl["spec"])
     n, T, k = wl["n"], wl["T"], args.k
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: torch's default (legacy) stream has handle 0, which
+    # sb_set_stream treats as "use the plan's own stream"
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
 
     rng = np.random.default_rng(12345 + rank)
     host_in = torch.empty(n + 2 * spec.r, dtype=torch.float64, pin_memory=True)
@@ -341,8 +344,12 @@ def run_gpu_arm(args):
                 p.upload(host_in.numpy())
                 p.run(T // 4)
                 tim = p.run(T)
-                sweep[str(kk)] = {"gstencil": n * T / (tim.device_ms * 1e-3) / 1e9,
-                                  "ms": tim.device_ms, "launches": tim.launches}
+                g = n * T / (tim.device_ms * 1e-3) / 1e9
+                hb = peaks["hbm_gbs"] * kk / ALG_BYTES_PER_POINT
+                sweep[str(kk)] = {"gstencil": g, "ms": tim.device_ms, "launches": tim.launches,
+                                  "roofline_gstencil": min(hb, fp_bound),
+                                  "binding": "hbm" if hb < fp_bound else "fp64",
+                                  "frac": g / min(hb, fp_bound)}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -45,10 +46,18 @@ int fail(int code, const char* fmt, ...) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
-constexpr int64_t kRightPad1D = 4096 + 1024;  // >= max lane span S + lead + RK + Q
+constexpr int64_t kRightPad1D = 4096 + 1024;  // >= last-chunk overrun (< 32*Q) + lead + RK + Q
 constexpr int kMaxS1D = 4096;
 
 enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2 };
+
+struct Sched1D {
+    int K = 0;
+    int blocks = 0;
+    int nchunks = 0;   // interior chunks
+    int nedge = 0;     // boundary chunks (edge kernel)
+    sb::Chunk1D* d_chunks = nullptr;
+};
 
 }  // namespace
 
@@ -69,9 +78,15 @@ struct sb_plan {
     bool uploaded = false;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t side_stream = nullptr;            // boundary work forked from `stream`
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int64_t* d_lin = nullptr;
     void* d_w = nullptr;
+    unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
+    std::vector<Sched1D> sched1d;
+    unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
+    int trace_n = 0;
     int kind = KK_GENERIC;
     int k = 1;
     int num_sms = 148;
@@ -161,43 +176,149 @@ int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
     return SB_OK;
 }
 
-template <typename T, int R, int K, bool FMA>
+// Tuning knobs (development only; defaults are the measured best).
+double env_double(const char* name, double dflt) {
+    const char* v = getenv(name);
+    return v ? atof(v) : dflt;
+}
+
+// Guided chunk schedule for the persistent 1D kernel.  Chunks are claimed in
+// list order: first one large chunk per warp (a fraction of the line), then
+// chunks shrinking with the remaining work so the tail is balanced, and last
+// the two minimum-size chunks touching the physical boundaries (they run the
+// slower EDGE path; a large one there was measured to hold a whole launch
+// back by ~50%).  S is a multiple of Q; the final chunk overruns n by
+// < 32*Q points (covered by the right pad).
+std::vector<sb::Chunk1D> guided_schedule_1d(int64_t n, int64_t warps, int Q, int64_t s_min,
+                                           bool phys_lo, bool phys_hi, int* n_edge) {
+    std::vector<sb::Chunk1D> main, edges;
+    auto mk = [&](int64_t start, int64_t S) {
+        sb::Chunk1D c;
+        c.start = start;
+        c.S = (int32_t)S;
+        c.pad = 0;
+        return c;
+    };
+    const int64_t edge = 32 * s_min;
+    const double frac = env_double("SB200_1D_FIRST_FRAC", 0.7);
+    const double div = env_double("SB200_1D_GUIDED_DIV", 2.0);
+    const int64_t fixed = (int64_t)env_double("SB200_1D_FIXED_S", 0);
+    if (n <= 3 * edge) {  // small line: minimum-size chunks, boundary ones on the edge path
+        for (int64_t pos = 0; pos < n; pos += edge) {
+            const bool e = (phys_lo && pos == 0) || (phys_hi && pos + edge >= n);
+            (e ? edges : main).push_back(mk(pos, s_min));
+        }
+    } else {
+        const int64_t lo = edge, hi = n - edge;
+        const int64_t first =
+            std::max<int64_t>(s_min, (int64_t)(frac * (double)(hi - lo) / (32.0 * warps)) / Q * Q);
+        int64_t pos = lo, issued = 0;
+        while (pos < hi) {
+            const int64_t rem = hi - pos;
+            int64_t S = issued < warps ? first : round_up((int64_t)(rem / (32 * warps * div)), Q);
+            if (fixed > 0) S = round_up(fixed, Q);
+            S = std::max<int64_t>(S, s_min);
+            S = std::min<int64_t>(S, kMaxS1D);
+            S = std::min<int64_t>(S, round_up((rem + 31) / 32, Q));
+            main.push_back(mk(pos, S));
+            pos += 32 * S;
+            issued++;
+        }
+        (phys_lo ? edges : main).push_back(mk(0, s_min));
+        if (pos < n) (phys_hi ? edges : main).push_back(mk(pos, round_up((n - pos + 31) / 32, Q)));
+    }
+    *n_edge = (int)edges.size();
+    main.insert(main.end(), edges.begin(), edges.end());
+    return main;
+}
+
+// ONE_PER_SMSP: one 4-warp CTA per SM (one warp per scheduler: no
+// arbitration between warps, up to 255 registers, deep cp.async ring).
+template <typename T, int R, int K, bool FMA, int MINB, int NST, bool ONE_PER_SMSP, bool DIAG = false>
 int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
-    using SH = sb::Fused1DShape<T>;
-    auto kern = sb::fused1d_kernel<T, R, K, FMA>;
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SH::SMEM_BYTES));
-    int blocks_per_sm = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, SH::WARPS * 32, SH::SMEM_BYTES));
-    blocks_per_sm = std::max(blocks_per_sm, 1);
-    const int64_t n = P->g.n[2];
-    const int64_t lanes_target = (int64_t)P->num_sms * blocks_per_sm * SH::WARPS * 32;
-    int64_t S = (n + lanes_target - 1) / lanes_target;
-    S = std::max<int64_t>(round_up(S, SH::Q), SH::Q * 4);
-    S = std::min<int64_t>(S, kMaxS1D);
+    using SH = sb::Fused1DShape<T, NST>;
+    auto kern = sb::fused1d_kernel<T, R, K, FMA, MINB, NST, DIAG>;
+    // one CTA per SM is enforced through the shared-memory request
+    const int smem = ONE_PER_SMSP ? std::max(SH::SMEM_BYTES, 120 * 1024) : SH::SMEM_BYTES;
+    Sched1D* sc = nullptr;
+    for (auto& e : P->sched1d)
+        if (e.K == K) sc = &e;
+    if (!sc) {
+        SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     (int)cudaSharedmemCarveoutMaxShared));
+        int blocks_per_sm = 0;
+        SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, SH::WARPS * 32, smem));
+        blocks_per_sm = std::max(blocks_per_sm, 1);
+        Sched1D e;
+        e.K = K;
+        e.blocks = P->num_sms * blocks_per_sm;
+        const int64_t warps = (int64_t)e.blocks * SH::WARPS;
+        int n_edge = 0;
+        auto chunks = guided_schedule_1d(P->g.n[2], warps, SH::Q,
+                                         (int64_t)env_double("SB200_1D_SMIN", 12 * SH::Q),
+                                         P->phys_lo, P->phys_hi, &n_edge);
+        e.nchunks = (int)chunks.size() - n_edge;
+        e.nedge = n_edge;
+        auto ekern = sb::fused1d_edge_kernel<T, R, K, FMA, NST, DIAG>;
+        SB_CUDA(cudaFuncSetAttribute(ekern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T)));
+        SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Chunk1D) * chunks.size()));
+        SB_CUDA(cudaMemcpy(e.d_chunks, chunks.data(), sizeof(sb::Chunk1D) * chunks.size(),
+                           cudaMemcpyHostToDevice));
+        P->sched1d.push_back(e);
+        sc = &P->sched1d.back();
+    }
     sb::Fused1DParams<T, R> prm;
     prm.src = src + P->g.origin;
     prm.dst = dst + P->g.origin;
-    prm.n = n;
-    prm.S = S;
-    prm.nlanes = (n + S - 1) / S;
+    prm.n = P->g.n[2];
+    prm.chunks = sc->d_chunks;
+    prm.nchunks = sc->nchunks;
+    prm.total_warps = sc->blocks * SH::WARPS;
+    prm.counter = P->d_counter;
+    prm.trace = nullptr;
+    if (getenv("SB200_TRACE")) {
+        if (!P->d_trace) SB_CUDA(cudaMalloc(&P->d_trace, sizeof(unsigned long long) * 4 * (1 << 20)));
+        if (sc->nchunks <= (1 << 20)) prm.trace = P->d_trace;
+        P->trace_n = sc->nchunks;
+    }
     prm.phys_lo = P->phys_lo;
     prm.phys_hi = P->phys_hi;
     for (int i = 0; i < 2 * R + 1; i++) prm.w[i] = (T)P->weights[i];
-    const int64_t warps = (prm.nlanes + 31) / 32;
-    const int64_t blocks = (warps + SH::WARPS - 1) / SH::WARPS;
-    kern<<<(unsigned)blocks, SH::WARPS * 32, SH::SMEM_BYTES, P->stream>>>(prm);
+    if (sc->nedge > 0) {  // fork: boundary chunks on the side stream, concurrently
+        SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
+        SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
+        sb::fused1d_edge_kernel<T, R, K, FMA, NST, DIAG><<<(unsigned)sc->nedge, 32,
+            (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T), P->side_stream>>>(prm);
+        SB_CUDA(cudaGetLastError());
+        SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+    }
+    kern<<<(unsigned)sc->blocks, SH::WARPS * 32, smem, P->stream>>>(prm);
     SB_CUDA(cudaGetLastError());
+    if (sc->nedge > 0) SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));  // join
     return SB_OK;
 }
 
 template <typename T, int R, bool FMA>
 int launch_fused1d_r(sb_plan* P, const T* src, T* dst, int k) {
+    static const int mode = (int)env_double("SB200_1D_MODE", 0);
     switch (k) {
-        case 1: return launch_fused1d_k<T, R, 1, FMA>(P, src, dst);
-        case 2: return launch_fused1d_k<T, R, 2, FMA>(P, src, dst);
-        case 4: return launch_fused1d_k<T, R, 4, FMA>(P, src, dst);
-        case 8: return launch_fused1d_k<T, R, 8, FMA>(P, src, dst);
-        case 16: return launch_fused1d_k<T, R, 16, FMA>(P, src, dst);
+        case 1: return launch_fused1d_k<T, R, 1, FMA, 1, 3, false>(P, src, dst);
+        case 2: return launch_fused1d_k<T, R, 2, FMA, 1, 3, false>(P, src, dst);
+        case 4: return launch_fused1d_k<T, R, 4, FMA, 1, 3, false>(P, src, dst);
+        case 8:
+            if (mode == 1) return launch_fused1d_k<T, R, 8, FMA, 1, 6, true>(P, src, dst);
+            if (mode == 2) return launch_fused1d_k<T, R, 8, FMA, 1, 3, false, true>(P, src, dst);
+            if (mode == 3) return launch_fused1d_k<T, R, 8, FMA, 1, 4, false>(P, src, dst);
+            if (mode == 4) return launch_fused1d_k<T, R, 8, FMA, 1, 5, false>(P, src, dst);
+            return launch_fused1d_k<T, R, 8, FMA, 1, 3, false>(P, src, dst);
+        case 16:
+            if (mode == 1) return launch_fused1d_k<T, R, 16, FMA, 1, 6, true>(P, src, dst);
+            if (mode == 2) return launch_fused1d_k<T, R, 16, FMA, 1, 3, false, true>(P, src, dst);
+            if (mode == 3) return launch_fused1d_k<T, R, 16, FMA, 1, 4, false>(P, src, dst);
+            if (mode == 4) return launch_fused1d_k<T, R, 16, FMA, 1, 5, false>(P, src, dst);
+            return launch_fused1d_k<T, R, 16, FMA, 1, 3, false>(P, src, dst);
         default: return fail(SB_ERR_ARG, "unsupported fused depth %d", k);
     }
 }
@@ -309,8 +430,15 @@ void sb_plan_destroy(sb_plan* P) {
         if (P->buf[i]) cudaFree(P->buf[i]);
     if (P->d_lin) cudaFree(P->d_lin);
     if (P->d_w) cudaFree(P->d_w);
+    if (P->d_counter) cudaFree(P->d_counter);
+    if (P->d_trace) cudaFree(P->d_trace);
+    for (auto& e : P->sched1d)
+        if (e.d_chunks) cudaFree(e.d_chunks);
     for (int i = 0; i < 2; i++)
         if (P->ev[i]) cudaEventDestroy(P->ev[i]);
+    if (P->fork_ev) cudaEventDestroy(P->fork_ev);
+    if (P->join_ev) cudaEventDestroy(P->join_ev);
+    if (P->side_stream) cudaStreamDestroy(P->side_stream);
     if (P->own_stream) cudaStreamDestroy(P->own_stream);
     delete P;
 }
@@ -438,6 +566,9 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     SB_CUDA_P(cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device));
     SB_CUDA_P(cudaStreamCreateWithFlags(&P->own_stream, cudaStreamNonBlocking));
     P->stream = P->own_stream;
+    SB_CUDA_P(cudaStreamCreateWithFlags(&P->side_stream, cudaStreamNonBlocking));
+    SB_CUDA_P(cudaEventCreateWithFlags(&P->fork_ev, cudaEventDisableTiming));
+    SB_CUDA_P(cudaEventCreateWithFlags(&P->join_ev, cudaEventDisableTiming));
     SB_CUDA_P(cudaEventCreate(&P->ev[0]));
     SB_CUDA_P(cudaEventCreate(&P->ev[1]));
     for (int i = 0; i < 2; i++) {
@@ -455,6 +586,8 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
         }
         lin[i] = o;
     }
+    SB_CUDA_P(cudaMalloc(&P->d_counter, 4 * sizeof(unsigned int)));
+    SB_CUDA_P(cudaMemset(P->d_counter, 0, 4 * sizeof(unsigned int)));
     SB_CUDA_P(cudaMalloc(&P->d_lin, sizeof(int64_t) * P->nw));
     SB_CUDA_P(cudaMemcpy(P->d_lin, lin.data(), sizeof(int64_t) * P->nw, cudaMemcpyHostToDevice));
     SB_CUDA_P(cudaMalloc(&P->d_w, P->es * P->nw));
@@ -533,6 +666,14 @@ int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
     SB_CUDA(cudaEventRecord(P->ev[1], P->stream));
     SB_CUDA(cudaEventSynchronize(P->ev[1]));
     SB_CUDA(cudaGetLastError());
+    if (P->d_trace && getenv("SB200_TRACE")) {  // debug: last launch's per-chunk trace
+        std::vector<unsigned long long> h((size_t)4 * P->trace_n);
+        SB_CUDA(cudaMemcpy(h.data(), P->d_trace, h.size() * 8, cudaMemcpyDeviceToHost));
+        if (FILE* f = fopen(getenv("SB200_TRACE"), "wb")) {
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+    }
     if (t) {
         float ms = 0.f;
         SB_CUDA(cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]));
