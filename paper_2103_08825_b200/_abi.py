@@ -10,7 +10,7 @@ import os
 from .core import GridError, SpecError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libsb200.so")
+LIB_PATH = os.environ.get("SB200_LIB") or os.path.join(_PKG, "lib", "libsb200.so")  # override: dev only
 
 SB_OK, SB_ERR_SPEC, SB_ERR_GRID, SB_ERR_ARG, SB_ERR_CUDA, SB_ERR_NOMEM, SB_ERR_STATE = 0, -1, -2, -3, -4, -5, -6
 SB_F64, SB_F32 = 0, 1

@@ -1,0 +1,312 @@
+// K3/K4 -- fused 3D sweep (r = 1 star 7-point or box 27-point), K time
+// steps per HBM round trip: 2.5D streaming along z with temporal blocking.
+//
+// Replaces the reference's 3D path, which has no blocking at all
+// (harness.py:127-136 runs 3D untiled) and sums the canonical offsets with
+// numpy passes (kernels.py:103-108).
+//
+// Structure (one work item = one xy tile x one z segment; persistent CTAs
+// claim items from an atomic queue):
+//  * level-0 planes arrive by TMA (cp.async.bulk.tensor.3d, mbarrier ring of
+//    NS0 slots, out-of-bounds boxes zero-filled) as a PW x PH box: the 64 x 32
+//    computed region plus one ring;
+//  * every level l = 1..K keeps, per thread, two pending partial-sum planes in
+//    registers (push form along z): when the level-(l-1) plane a arrives, its
+//    in-plane neighbourhood is read from shared memory ONCE and folded into
+//    output planes a+1 (dz=-1, first terms), a (dz=0) and a-1 (dz=+1, last
+//    terms -> complete).  Each output therefore still sums its terms in
+//    canonical (dz, dy, dx) lexicographic order (bit-exact in EXACT mode);
+//  * the completed level-l plane goes to a shared plane read by level l+1
+//    in the same step; level K goes to global memory.
+//  * 256 threads x (2 x 4) points cover the 64 x 32 computed region at every
+//    level; valid data shrinks by one ring per level, so the output tile is
+//    (66 - 2K) x (34 - 2K) (overlapped-tile recompute in x and y).
+//
+// Boundaries: an emitted value at a position outside the interior on a
+// physical side is replaced by the Dirichlet halo value (read from global;
+// the halo is the same at every level), beyond the halo shell by 0 (never
+// used by a valid output).  Slab (ghost) sides along z are computed normally.
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+
+#ifndef SB_F3_DEBUG
+#define SB_F3_DEBUG 0   // development bisection switches (0 = production)
+#endif
+
+namespace sb {
+
+constexpr int F3_CW = 64;        // computed region width (x)
+constexpr int F3_CH = 32;        // computed region height (y)
+constexpr int F3_PW = 68;        // shared plane width: ring + region + pad (16 B rows)
+constexpr int F3_PH = 34;        // shared plane height: ring + region + ring
+constexpr int F3_THREADS = 256;  // 32 (x) x 8 (y) threads, 2 x 4 points each
+constexpr int F3_NS0 = 4;        // TMA ring depth (level-0 planes)
+
+// Plane stride in elements: TMA destinations must be 128 B aligned.
+template <typename T>
+struct F3Plane {
+    static constexpr int ELEMS = ((F3_PW * F3_PH * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
+    static constexpr unsigned BOX_BYTES = F3_PW * F3_PH * sizeof(T);
+};
+template <typename T, int K>
+constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T>::ELEMS * (int)sizeof(T) + 128; }
+
+template <typename T>
+struct Fused3DParams {
+    const T* src;            // buffer bases (element (z,y,x) at origin + z*sz + y*sy + x)
+    T* dst;
+    int64_t origin, sz, sy;
+    int nx, ny, nz;
+    int ax, ry, hz;          // allocation coordinates of interior (0,0,0): col, row, plane
+    int phys_lo, phys_hi;    // z sides: physical halo (1) or ghost (0)
+    int ghost_lo, ghost_hi;  // ghost depth on slab sides (0 on physical sides)
+    int tiles_x, tiles_y, nseg, lz;
+    int items;
+    int total_ctas;
+    unsigned int* counter;   // [0] next item, [1] retired CTAs
+    T w[27];                 // w[(dz+1)*9 + (dy+1)*3 + (dx+1)]; star uses 7 entries
+};
+
+// Output tile geometry.  The TMA box's first column (x0 - K) must be 16 B
+// aligned (measured: an unaligned innermost coordinate traps with "illegal
+// instruction"), so the tile pitch is a multiple of the 16 B vector and the
+// tiles start at X0 <= 0 with X0 == K (mod VEC); columns x < 0 are not stored.
+template <typename T, int K>
+struct F3Tile {
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int TXO = ((F3_CW - 2 * (K - 1)) / VEC) * VEC;   // output tile width
+    static constexpr int TYO = F3_CH - 2 * (K - 1);                   // output tile height
+    static constexpr int X0 = (K % VEC == 0) ? 0 : (K % VEC) - VEC;  // first tile's x origin
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Fold one arriving plane into a level's pending sums (push form along z).
+// v[6][4]: rows 4ty-1..4ty+4, cols 2tx-1..2tx+2 of the computed region.
+template <typename T, bool BOX, bool FMA>
+__device__ __forceinline__ void f3_push(const T (&v)[6][4], T (&Pm)[4][2], T (&P0)[4][2], T (&done)[4][2],
+                                        const T* w) {
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            // dz = +1 terms complete output plane a-1
+            T acc = Pm[i][j];
+            if (BOX) {
+#pragma unroll
+                for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; dx++)
+                        acc = acc_term<T, FMA>(acc, w[18 + (dy + 1) * 3 + (dx + 1)], v[i + 1 + dy][j + 1 + dx]);
+            } else {
+                acc = acc_term<T, FMA>(acc, w[22], v[i + 1][j + 1]);
+            }
+            done[i][j] = acc;
+            // dz = 0 terms: output plane a
+            acc = P0[i][j];
+            if (BOX) {
+#pragma unroll
+                for (int dy = -1; dy <= 1; dy++)
+#pragma unroll
+                    for (int dx = -1; dx <= 1; dx++)
+                        acc = acc_term<T, FMA>(acc, w[9 + (dy + 1) * 3 + (dx + 1)], v[i + 1 + dy][j + 1 + dx]);
+            } else {
+                acc = acc_term<T, FMA>(acc, w[10], v[i][j + 1]);      // (0,-1,0)
+                acc = acc_term<T, FMA>(acc, w[12], v[i + 1][j]);      // (0,0,-1)
+                acc = acc_term<T, FMA>(acc, w[13], v[i + 1][j + 1]);  // (0,0,0)
+                acc = acc_term<T, FMA>(acc, w[14], v[i + 1][j + 2]);  // (0,0,1)
+                acc = acc_term<T, FMA>(acc, w[16], v[i + 2][j + 1]);  // (0,1,0)
+            }
+            Pm[i][j] = acc;
+            // dz = -1 terms start output plane a+1 (the canonical first term)
+            if (BOX) {
+                acc = acc_first<T, FMA>(w[0], v[i][j]);
+#pragma unroll
+                for (int q = 1; q < 9; q++)
+                    acc = acc_term<T, FMA>(acc, w[q], v[i + q / 3][j + q % 3]);
+            } else {
+                acc = acc_first<T, FMA>(w[4], v[i + 1][j + 1]);
+            }
+            P0[i][j] = acc;
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void f3_read(const T* plane, int tx, int ty, T (&v)[6][4]) {
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+        const T* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
+        if (sizeof(T) == 8) {
+            const double2 a = *reinterpret_cast<const double2*>(row);
+            const double2 b = *reinterpret_cast<const double2*>(row + 2);
+            v[r][0] = (T)a.x; v[r][1] = (T)a.y; v[r][2] = (T)b.x; v[r][3] = (T)b.y;
+        } else {
+            const float2 a = *reinterpret_cast<const float2*>(row);
+            const float2 b = *reinterpret_cast<const float2*>(row + 2);
+            v[r][0] = (T)a.x; v[r][1] = (T)a.y; v[r][2] = (T)b.x; v[r][3] = (T)b.y;
+        }
+    }
+}
+
+template <typename T, bool BOX, int K, bool FMA>
+__global__ void __launch_bounds__(F3_THREADS, 1)
+fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
+    constexpr int PLANE = F3Plane<T>::ELEMS;
+    constexpr unsigned PLANE_BYTES = F3Plane<T>::BOX_BYTES;
+    using TL = F3Tile<T, K>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* s0 = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));  // NS0 level-0 slots
+    T* sl = s0 + F3_NS0 * PLANE;                       // levels 1..K-1, one plane each
+    __shared__ uint64_t bar[F3_NS0];
+    __shared__ unsigned s_item;
+
+    const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = tid >> 5;
+    if (tid == 0) {
+        for (int i = 0; i < F3_NS0; i++) mbar_init(&bar[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#if SB_F3_DEBUG != 1
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+#endif
+    }
+    __syncthreads();
+
+    unsigned gstep = 0;   // CTA-lifetime step counter: slot = g % NS0, parity = (g / NS0) & 1
+    for (;;) {
+        if (tid == 0) s_item = atomicAdd(&P.counter[0], 1u);
+        __syncthreads();
+        const unsigned item = s_item;
+        if (item >= (unsigned)P.items) break;
+        const int tix = item % P.tiles_x;
+        const int tiy = (item / P.tiles_x) % P.tiles_y;
+        const int seg = item / (P.tiles_x * P.tiles_y);
+        const int x0 = TL::X0 + tix * TL::TXO, y0 = tiy * TL::TYO;   // output tile origin
+        const int xc = x0 - (K - 1), yc = y0 - (K - 1);         // computed region origin
+        int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);      // output planes
+        // slab sides: the first/last segment also produces nothing below 0 / above nz
+        const int p_first = zs0 - K;
+        const int M = (zs1 - zs0) + 2 * K;                      // level-0 arrivals
+
+        auto issue = [&](int t) {
+            const unsigned g = gstep + t;
+            uint64_t* b = &bar[g % F3_NS0];
+            mbar_expect_tx(b, PLANE_BYTES);
+#if SB_F3_DEBUG == 6
+            tma_load_3d(s0 + (g % F3_NS0) * PLANE, &tmap, b, 0, 0, 0);
+#else
+            tma_load_3d(s0 + (g % F3_NS0) * PLANE, &tmap, b, P.ax + x0 - K, P.ry + y0 - K,
+                        P.hz + p_first + t);
+#endif
+        };
+        if (tid == 0 && SB_F3_DEBUG != 4)
+            for (int t = 0; t < F3_NS0 && t < M && (SB_F3_DEBUG != 7 || t < 1); t++) issue(t);
+
+        T Pm[K][4][2], P0[K][4][2];
+#pragma unroll
+        for (int l = 0; l < K; l++)
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 2; j++) Pm[l][i][j] = P0[l][i][j] = T(0);
+
+        for (int t = 0; t < M; t++) {
+            const unsigned g = gstep + t;
+            if (SB_F3_DEBUG != 4 && !(SB_F3_DEBUG == 5 && t >= F3_NS0) && !(SB_F3_DEBUG == 7 && t >= 1))
+                mbar_wait(&bar[g % F3_NS0], (g / F3_NS0) & 1);
+            const int a0 = p_first + t;   // level-0 plane that arrived
+#pragma unroll
+            for (int l = 1; l <= K; l++) {
+                const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE : sl + (l - 2) * PLANE;
+                T v[6][4];
+                f3_read<T>(in, tx, ty, v);
+                T done[4][2];
+                f3_push<T, BOX, FMA>(v, Pm[l - 1], P0[l - 1], done, P.w);
+                const int zc = a0 - l;    // completed level-l plane
+                const bool z_out = (P.phys_lo && zc < 0) || (P.phys_hi && zc >= P.nz);
+                const bool z_shell = zc >= -1 && zc <= P.nz;
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int y = yc + 4 * ty + i;
+#pragma unroll
+                    for (int j = 0; j < 2; j++) {
+                        const int x = xc + 2 * tx + j;
+                        const bool out = z_out || x < 0 || x >= P.nx || y < 0 || y >= P.ny;
+                        if (out) {   // Dirichlet halo: same value at every level
+                            const bool shell = z_shell && x >= -1 && x <= P.nx && y >= -1 && y <= P.ny;
+#if SB_F3_DEBUG == 2
+                            done[i][j] = T(0);
+                            (void)shell;
+#else
+                            done[i][j] = shell ? P.src[P.origin + (int64_t)zc * P.sz + (int64_t)y * P.sy + x] : T(0);
+#endif
+                        }
+                    }
+                }
+                if (l < K) {
+                    T* o = sl + (l - 1) * PLANE;
+#pragma unroll
+                    for (int i = 0; i < 4; i++)
+#pragma unroll
+                        for (int j = 0; j < 2; j++) o[(4 * ty + i + 1) * F3_PW + 2 * tx + j + 1] = done[i][j];
+                } else if (zc >= zs0 && zc < zs1) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const int ri = 4 * ty + i - (K - 1);
+                        const int y = y0 + ri;
+                        if (ri < 0 || ri >= TL::TYO || y >= P.ny) continue;
+#pragma unroll
+                        for (int j = 0; j < 2; j++) {
+                            const int cj = 2 * tx + j - (K - 1);
+                            const int x = x0 + cj;
+                            if (SB_F3_DEBUG != 3 && cj >= 0 && cj < TL::TXO && x >= 0 && x < P.nx)
+                                P.dst[P.origin + (int64_t)zc * P.sz + (int64_t)y * P.sy + x] = done[i][j];
+                        }
+                    }
+                }
+                if (l < K || K == 1) __syncthreads();
+                if (SB_F3_DEBUG != 4 && SB_F3_DEBUG != 5 && SB_F3_DEBUG != 7 && l == 1 && tid == 0 && t + F3_NS0 < M)
+                    issue(t + F3_NS0);   // slot consumed by level 1
+            }
+            if (K > 1) __syncthreads();   // level K read sl[K-2] before the next step rewrites it
+        }
+        gstep += M;
+    }
+    if (tid == 0) {
+        const unsigned retired = atomicAdd(&P.counter[1], 1u);
+        if (retired == (unsigned)P.total_ctas - 1) {
+            atomicExch(&P.counter[0], 0u);
+            atomicExch(&P.counter[1], 0u);
+        }
+    }
+}
+
+}  // namespace sb

@@ -21,6 +21,7 @@
 #include "../../include/sb200.h"
 #include "common.cuh"
 #include "fused1d.cuh"
+#include "fused3d.cuh"
 #include "generic.cuh"
 
 namespace {
@@ -49,7 +50,7 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 constexpr int64_t kRightPad1D = 4096 + 1024;  // >= last-chunk overrun (< 32*Q) + lead + RK + Q
 constexpr int kMaxS1D = 4096;
 
-enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2 };
+enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2, KK_FUSED3D = 3 };
 
 struct Sched1D {
     int K = 0;
@@ -85,6 +86,7 @@ struct sb_plan {
     void* d_w = nullptr;
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<Sched1D> sched1d;
+    CUtensorMap tmap[2];                   // TMA descriptors of the two buffers (3D)
     unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
     int trace_n = 0;
     int kind = KK_GENERIC;
@@ -148,15 +150,29 @@ int validate_problem(const sb_problem* p) {
     return SB_OK;
 }
 
-bool fused1d_supported(const sb_plan* P) { return P->d == 1 && (P->r == 1 || P->r == 2); }
+// Fused kernel available for this stencil class (0 = none).
+int fused_kind(const sb_plan* P) {
+    if (P->d == 1 && (P->r == 1 || P->r == 2)) return KK_FUSED1D;
+    if (P->d == 3 && P->r == 1) return KK_FUSED3D;   // 7-point star or 27-point box
+    return 0;
+}
 
-// Supported fused depths (template instantiations).
-bool fused_k_ok(int k) { return k == 1 || k == 2 || k == 4 || k == 8 || k == 16; }
+// Supported fused depths (template instantiations) per kernel.
+bool fused_k_ok(int kind, int k) {
+    if (kind == KK_FUSED3D) return k >= 1 && k <= 4;
+    return k == 1 || k == 2 || k == 4 || k == 8 || k == 16;
+}
 
-int largest_fused_k(int64_t steps, int kmax) {
+int largest_fused_k(int kind, int64_t steps, int kmax) {
+    if (kind == KK_FUSED3D) return (int)std::min<int64_t>(steps, kmax);
     int k = 1;
     while (k * 2 <= kmax && k * 2 <= steps) k *= 2;
     return k;
+}
+
+int default_k(int kind, const sb_plan* P) {
+    if (kind == KK_FUSED3D) return P->shape == SB_BOX ? 2 : 4;
+    return 16;
 }
 
 // ---------------------------------------------------------------- launches
@@ -329,6 +345,99 @@ int launch_fused1d(sb_plan* P, const T* src, T* dst, int k) {
     return launch_fused1d_r<T, 2, FMA>(P, src, dst, k);
 }
 
+// ---------------------------------------------------------------- 3D
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// One TMA descriptor per device buffer: a 3D view (cols, rows, planes) of
+// the whole allocation; boxes of F3_PW x F3_PH x 1, OOB elements zero-filled.
+int make_tensor_maps(sb_plan* P) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto encode = reinterpret_cast<EncodeTiledFn>(fn);
+    const int64_t rows = P->dims[1] + 2 * P->r;
+    const int64_t planes = P->hlo + P->dims[0] + P->hhi;
+    cuuint64_t dims[3] = {(cuuint64_t)P->px, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)(P->px * P->es), (cuuint64_t)(rows * P->px * P->es)};
+    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)sb::F3_PH, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = P->dtype == SB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    for (int b = 0; b < 2; b++) {
+        CUresult r = encode(&P->tmap[b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    return SB_OK;
+}
+
+template <typename T, bool BOX, int K, bool FMA>
+int launch_fused3d_k(sb_plan* P, int src_idx) {
+    using TL = sb::F3Tile<T, K>;
+    auto kern = sb::fused3d_kernel<T, BOX, K, FMA>;
+    const int smem = sb::f3_smem_bytes<T, K>();
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3_THREADS, smem));
+    occ = std::max(occ, 1);
+    sb::Fused3DParams<T> prm;
+    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
+    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
+    prm.origin = P->g.origin;
+    prm.sz = P->g.sz;
+    prm.sy = P->g.sy;
+    prm.nz = (int)P->dims[0];
+    prm.ny = (int)P->dims[1];
+    prm.nx = (int)P->dims[2];
+    prm.ax = (int)(P->g.origin % P->g.sy);
+    prm.ry = P->r;
+    prm.hz = (int)P->hlo;
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    prm.ghost_lo = P->phys_lo ? 0 : (int)P->hlo;
+    prm.ghost_hi = P->phys_hi ? 0 : (int)P->hhi;
+    prm.tiles_x = (int)((P->dims[2] - TL::X0 + TL::TXO - 1) / TL::TXO);
+    prm.tiles_y = (int)((P->dims[1] + TL::TYO - 1) / TL::TYO);
+    const int ctas_max = P->num_sms * occ;
+    const int tiles = prm.tiles_x * prm.tiles_y;
+    const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", 6.0);
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(seg_env * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
+    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    prm.items = tiles * prm.nseg;
+    prm.total_ctas = std::min(ctas_max, prm.items);
+    prm.counter = P->d_counter;
+    for (int i = 0; i < 27; i++) prm.w[i] = T(0);
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[3 * i];
+        prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
+    }
+    kern<<<(unsigned)prm.total_ctas, sb::F3_THREADS, smem, P->stream>>>(P->tmap[src_idx], prm);
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, bool BOX, bool FMA>
+int launch_fused3d_b(sb_plan* P, int src_idx, int k) {
+    switch (k) {
+        case 1: return launch_fused3d_k<T, BOX, 1, FMA>(P, src_idx);
+        case 2: return launch_fused3d_k<T, BOX, 2, FMA>(P, src_idx);
+        case 3: return launch_fused3d_k<T, BOX, 3, FMA>(P, src_idx);
+        case 4: return launch_fused3d_k<T, BOX, 4, FMA>(P, src_idx);
+        default: return fail(SB_ERR_ARG, "unsupported 3D fused depth %d", k);
+    }
+}
+
+template <typename T, bool FMA>
+int launch_fused3d(sb_plan* P, int src_idx, int k) {
+    if (P->shape == SB_BOX) return launch_fused3d_b<T, true, FMA>(P, src_idx, k);
+    return launch_fused3d_b<T, false, FMA>(P, src_idx, k);
+}
+
 // One launch advancing k levels from buf[cur] into buf[cur^1].
 template <typename T, bool FMA>
 int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
@@ -337,6 +446,8 @@ int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
     int rc;
     if (P->kind == KK_FUSED1D) {
         rc = launch_fused1d<T, FMA>(P, src, dst, k);
+    } else if (P->kind == KK_FUSED3D) {
+        rc = launch_fused3d<T, FMA>(P, P->cur, k);
     } else {
         // generic: one level; on slab sides the valid range shrinks by r per level
         const int64_t n0 = P->dims[0];
@@ -364,7 +475,7 @@ int run_steps(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
     }
     if (slab) {
         // A slab plan runs one fused launch per exchange interval.
-        if (fused_k_ok((int)steps)) {
+        if (fused_k_ok(P->kind, (int)steps)) {
             *k_used = (int)steps;
             return launch_one<T, FMA>(P, (int)steps, 0, launches);
         }
@@ -377,7 +488,7 @@ int run_steps(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
     }
     *k_used = P->k;
     while (done < steps) {
-        const int kk = (steps - done >= P->k) ? P->k : largest_fused_k(steps - done, P->k);
+        const int kk = (steps - done >= P->k) ? P->k : largest_fused_k(P->kind, steps - done, P->k);
         int rc = launch_one<T, FMA>(P, kk, 0, launches);
         if (rc != SB_OK) return rc;
         done += kk;
@@ -396,6 +507,7 @@ int dispatch_run(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
 
 const char* kernel_name(const sb_plan* P) {
     if (P->kind == KK_FUSED1D) return "fused1d_kernel";
+    if (P->kind == KK_FUSED3D) return "fused3d_kernel";
     return "generic_step_kernel";
 }
 
@@ -469,17 +581,18 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     P->es = (P->dtype == SB_F64) ? 8 : 4;
 
     // ---- kernel choice
-    const bool fused_ok = fused1d_supported(P);
-    if (prob->kernel == SB_KERNEL_FUSED && !fused_ok) {
+    const int fk = fused_kind(P);
+    if (prob->kernel == SB_KERNEL_FUSED && !fk) {
         delete P;
         return fail(SB_ERR_ARG, "no fused kernel for d=%d r=%d shape=%d", prob->d, prob->r, prob->shape);
     }
-    if (prob->kernel != SB_KERNEL_GENERIC && fused_ok) {
-        P->kind = KK_FUSED1D;
-        P->k = prob->k > 0 ? prob->k : 8;
-        if (!fused_k_ok(P->k)) {
+    if (prob->kernel != SB_KERNEL_GENERIC && fk) {
+        P->kind = fk;
+        P->k = prob->k > 0 ? prob->k : default_k(fk, P);
+        if (!fused_k_ok(fk, P->k)) {
             delete P;
-            return fail(SB_ERR_ARG, "fused depth k=%d unsupported (1, 2, 4, 8, 16)", prob->k);
+            return fail(SB_ERR_ARG, "fused depth k=%d unsupported by the %s kernel", prob->k,
+                        fk == KK_FUSED3D ? "3D (1..4)" : "1D (1, 2, 4, 8, 16)");
         }
     } else {
         P->kind = KK_GENERIC;
@@ -487,7 +600,7 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     }
     if (!(P->phys_lo && P->phys_hi)) {
         // slab: a launch of depth k needs ghost depth >= r*k on slab sides
-        if (P->kind == KK_FUSED1D && (int64_t)P->r * P->k > std::min(P->phys_lo ? INT32_MAX : P->hlo,
+        if (P->kind != KK_GENERIC && (int64_t)P->r * P->k > std::min(P->phys_lo ? INT32_MAX : P->hlo,
                                                                       P->phys_hi ? INT32_MAX : P->hhi)) {
             delete P;
             return fail(SB_ERR_GRID, "ghost depth must be >= r*k = %d", P->r * P->k);
@@ -596,6 +709,13 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     } else {
         std::vector<float> wf(P->weights.begin(), P->weights.end());
         SB_CUDA_P(cudaMemcpy(P->d_w, wf.data(), 4 * P->nw, cudaMemcpyHostToDevice));
+    }
+    if (P->kind == KK_FUSED3D) {
+        const int trc = make_tensor_maps(P);
+        if (trc != SB_OK) {
+            sb_plan_destroy(P);
+            return trc;
+        }
     }
     SB_CUDA_P(cudaStreamSynchronize(P->stream));
 #undef SB_CUDA_P

@@ -176,3 +176,58 @@ def test_plan_reuse_and_timing():
     want_mid = oracle(spec, box, 20)
     assert np_oracle.max_rel_error(mid, want_mid) <= FP64_TOL
     assert np_oracle.max_rel_error(end, oracle(spec, want_mid, 20)) <= FP64_TOL
+
+
+# --- fused 3D kernel (TMA-fed 2.5D temporal blocking) ---------------------------
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+@pytest.mark.parametrize("dims", [(3, 5, 7), (9, 40, 70), (37, 33, 130)])
+def test_fused3d_every_depth_exact(cfg, k, dims):
+    spec = config_spec(cfg)
+    box = seeded_box(dims, 1, seed=sum(dims) + k)
+    T = 7                                    # not a multiple of k for k in {2,3,4}
+    got = sweep(spec, box, T, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, T).tobytes()
+
+
+@pytest.mark.parametrize("cfg,k", [("c4", 4), ("c5", 2)])
+def test_fused3d_halo_zero_exact(cfg, k):
+    spec = config_spec(cfg)
+    box = seeded_box((20, 70, 66), 1, seed=5, halo="zero")
+    got = sweep(spec, box, 9, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, 9).tobytes()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_fused3d_fp32(k):
+    spec = config_spec("c5")
+    box32 = seeded_box((30, 70, 130), 1, seed=11).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 12)
+    got = sweep(spec, box32, 12, arith="fma", kernel="fused", k=k)
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+def test_c5_full_size_fma():
+    spec = config_spec("c5")
+    box = seeded_box((768, 768, 768), 1)
+    got = sweep(spec, box, 4, arith="fma", k=2)
+    want = oracle(spec, box, 4)
+    assert np_oracle.max_rel_error(got, want) <= FP64_TOL
+
+
+def test_c4_full_size_exact():
+    spec = config_spec("c4")
+    box = seeded_box((512, 512, 512), 1, halo="zero")
+    got = sweep(spec, box, 8, arith="exact", k=4)
+    assert got.tobytes() == oracle(spec, box, 8).tobytes()
+
+
+def test_c5_full_size_fp32():
+    spec = config_spec("c5")
+    box32 = seeded_box((768, 768, 768), 1, seed=2).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 4)
+    got = sweep(spec, box32, 4, arith="fma", k=2)
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
