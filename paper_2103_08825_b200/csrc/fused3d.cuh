@@ -51,7 +51,7 @@ struct F3Plane {
     static constexpr unsigned BOX_BYTES = F3_PW * F3_PH * sizeof(T);
 };
 template <typename T, int K>
-constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T>::ELEMS * (int)sizeof(T) + 128; }
+constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T>::ELEMS * (int)sizeof(T); }
 
 template <typename T>
 struct Fused3DParams {
@@ -111,53 +111,62 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 
 // Fold one arriving plane into a level's pending sums (push form along z).
 // v[6][4]: rows 4ty-1..4ty+4, cols 2tx-1..2tx+2 of the computed region.
+// Term-major order: each output still receives its terms in canonical
+// (dy, dx) order within a dz group, but consecutive FMAs in the instruction
+// stream belong to the 8 independent points (ILP 8 instead of one chain).
 template <typename T, bool BOX, bool FMA>
 __device__ __forceinline__ void f3_push(const T (&v)[6][4], T (&Pm)[4][2], T (&P0)[4][2], T (&done)[4][2],
                                         const T* w) {
+    T nx[4][2];
+    if (BOX) {
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+        for (int q = 0; q < 9; q++) {
+            const int dy = q / 3 - 1, dx = q % 3 - 1;
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const T x = v[i + 1 + dy][j + 1 + dx];
+                    Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[18 + q], x);      // dz=+1: completes a-1
+                    P0[i][j] = acc_term<T, FMA>(P0[i][j], w[9 + q], x);       // dz= 0: plane a
+                    nx[i][j] = q == 0 ? acc_first<T, FMA>(w[0], x)            // dz=-1: starts a+1
+                                      : acc_term<T, FMA>(nx[i][j], w[q], x);
+                }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) {
+                Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[22], v[i + 1][j + 1]);   // (1,0,0)
+                P0[i][j] = acc_term<T, FMA>(P0[i][j], w[10], v[i][j + 1]);       // (0,-1,0)
+                nx[i][j] = acc_first<T, FMA>(w[4], v[i + 1][j + 1]);             // (-1,0,0)
+            }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[12], v[i + 1][j]);      // (0,0,-1)
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[13], v[i + 1][j + 1]);  // (0,0,0)
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[14], v[i + 1][j + 2]);  // (0,0,1)
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[16], v[i + 2][j + 1]);  // (0,1,0)
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++)
 #pragma unroll
         for (int j = 0; j < 2; j++) {
-            // dz = +1 terms complete output plane a-1
-            T acc = Pm[i][j];
-            if (BOX) {
-#pragma unroll
-                for (int dy = -1; dy <= 1; dy++)
-#pragma unroll
-                    for (int dx = -1; dx <= 1; dx++)
-                        acc = acc_term<T, FMA>(acc, w[18 + (dy + 1) * 3 + (dx + 1)], v[i + 1 + dy][j + 1 + dx]);
-            } else {
-                acc = acc_term<T, FMA>(acc, w[22], v[i + 1][j + 1]);
-            }
-            done[i][j] = acc;
-            // dz = 0 terms: output plane a
-            acc = P0[i][j];
-            if (BOX) {
-#pragma unroll
-                for (int dy = -1; dy <= 1; dy++)
-#pragma unroll
-                    for (int dx = -1; dx <= 1; dx++)
-                        acc = acc_term<T, FMA>(acc, w[9 + (dy + 1) * 3 + (dx + 1)], v[i + 1 + dy][j + 1 + dx]);
-            } else {
-                acc = acc_term<T, FMA>(acc, w[10], v[i][j + 1]);      // (0,-1,0)
-                acc = acc_term<T, FMA>(acc, w[12], v[i + 1][j]);      // (0,0,-1)
-                acc = acc_term<T, FMA>(acc, w[13], v[i + 1][j + 1]);  // (0,0,0)
-                acc = acc_term<T, FMA>(acc, w[14], v[i + 1][j + 2]);  // (0,0,1)
-                acc = acc_term<T, FMA>(acc, w[16], v[i + 2][j + 1]);  // (0,1,0)
-            }
-            Pm[i][j] = acc;
-            // dz = -1 terms start output plane a+1 (the canonical first term)
-            if (BOX) {
-                acc = acc_first<T, FMA>(w[0], v[i][j]);
-#pragma unroll
-                for (int q = 1; q < 9; q++)
-                    acc = acc_term<T, FMA>(acc, w[q], v[i + q / 3][j + q % 3]);
-            } else {
-                acc = acc_first<T, FMA>(w[4], v[i + 1][j + 1]);
-            }
-            P0[i][j] = acc;
+            done[i][j] = Pm[i][j];
+            Pm[i][j] = P0[i][j];
+            P0[i][j] = nx[i][j];
         }
-    }
 }
 
 template <typename T>
@@ -177,14 +186,14 @@ __device__ __forceinline__ void f3_read(const T* plane, int tx, int ty, T (&v)[6
     }
 }
 
-template <typename T, bool BOX, int K, bool FMA>
-__global__ void __launch_bounds__(F3_THREADS, 1)
+template <typename T, bool BOX, int K, bool FMA, int MINB = 1>
+__global__ void __launch_bounds__(F3_THREADS, MINB)
 fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
     constexpr int PLANE = F3Plane<T>::ELEMS;
     constexpr unsigned PLANE_BYTES = F3Plane<T>::BOX_BYTES;
     using TL = F3Tile<T, K>;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* s0 = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));  // NS0 level-0 slots
+    extern __shared__ __align__(1024) unsigned char smem3d[];   // TMA destinations: 128 B aligned
+    T* s0 = reinterpret_cast<T*>(smem3d);              // NS0 level-0 slots
     T* sl = s0 + F3_NS0 * PLANE;                       // levels 1..K-1, one plane each
     __shared__ uint64_t bar[F3_NS0];
     __shared__ unsigned s_item;
@@ -211,6 +220,19 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         const int seg = item / (P.tiles_x * P.tiles_y);
         const int x0 = TL::X0 + tix * TL::TXO, y0 = tiy * TL::TYO;   // output tile origin
         const int xc = x0 - (K - 1), yc = y0 - (K - 1);         // computed region origin
+        // per-thread masks of its 8 points outside the x/y interior / on the halo shell,
+        // and their in-plane offsets (for the Dirichlet values)
+        unsigned out_mask = 0, shell_mask = 0;
+        int64_t hoff[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int y = yc + 4 * ty + (q >> 1), x = xc + 2 * tx + (q & 1);
+            const bool out = x < 0 || x >= P.nx || y < 0 || y >= P.ny;
+            const bool shell = x >= -1 && x <= P.nx && y >= -1 && y <= P.ny;
+            out_mask |= (unsigned)out << q;
+            shell_mask |= (unsigned)shell << q;
+            hoff[q] = P.origin + (int64_t)y * P.sy + x;
+        }
         int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);      // output planes
         // slab sides: the first/last segment also produces nothing below 0 / above nz
         const int p_first = zs0 - K;
@@ -252,24 +274,19 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                 f3_push<T, BOX, FMA>(v, Pm[l - 1], P0[l - 1], done, P.w);
                 const int zc = a0 - l;    // completed level-l plane
                 const bool z_out = (P.phys_lo && zc < 0) || (P.phys_hi && zc >= P.nz);
-                const bool z_shell = zc >= -1 && zc <= P.nz;
+                if (z_out) {   // uniform: a physical halo plane, every value is Dirichlet
+                    const bool z_shell = zc >= -1 && zc <= P.nz;
 #pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const int y = yc + 4 * ty + i;
-#pragma unroll
-                    for (int j = 0; j < 2; j++) {
-                        const int x = xc + 2 * tx + j;
-                        const bool out = z_out || x < 0 || x >= P.nx || y < 0 || y >= P.ny;
-                        if (out) {   // Dirichlet halo: same value at every level
-                            const bool shell = z_shell && x >= -1 && x <= P.nx && y >= -1 && y <= P.ny;
-#if SB_F3_DEBUG == 2
-                            done[i][j] = T(0);
-                            (void)shell;
-#else
-                            done[i][j] = shell ? P.src[P.origin + (int64_t)zc * P.sz + (int64_t)y * P.sy + x] : T(0);
-#endif
-                        }
+                    for (int q = 0; q < 8; q++) {
+                        T hv = T(0);
+                        if (z_shell && ((shell_mask >> q) & 1)) hv = P.src[hoff[q] + (int64_t)zc * P.sz];
+                        done[q >> 1][q & 1] = hv;
                     }
+                } else if (out_mask) {   // only threads owning points outside the x/y interior
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        if ((out_mask >> q) & 1)
+                            done[q >> 1][q & 1] = ((shell_mask >> q) & 1) ? P.src[hoff[q] + (int64_t)zc * P.sz] : T(0);
                 }
                 if (l < K) {
                     T* o = sl + (l - 1) * PLANE;

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "fused1d.cuh"
 #include "fused3d.cuh"
+#include "fused2d.cuh"
 #include "generic.cuh"
 
 namespace {
@@ -50,7 +51,7 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 constexpr int64_t kRightPad1D = 4096 + 1024;  // >= last-chunk overrun (< 32*Q) + lead + RK + Q
 constexpr int kMaxS1D = 4096;
 
-enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2, KK_FUSED3D = 3 };
+enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2, KK_FUSED3D = 3, KK_FUSED2D = 4 };
 
 struct Sched1D {
     int K = 0;
@@ -154,12 +155,14 @@ int validate_problem(const sb_problem* p) {
 int fused_kind(const sb_plan* P) {
     if (P->d == 1 && (P->r == 1 || P->r == 2)) return KK_FUSED1D;
     if (P->d == 3 && P->r == 1) return KK_FUSED3D;   // 7-point star or 27-point box
+    if (P->d == 2 && P->r == 1) return KK_FUSED2D;   // 5-point star or 9-point box
     return 0;
 }
 
 // Supported fused depths (template instantiations) per kernel.
 bool fused_k_ok(int kind, int k) {
     if (kind == KK_FUSED3D) return k >= 1 && k <= 4;
+    if (kind == KK_FUSED2D) return k == 1 || k == 2 || k == 4 || k == 8;
     return k == 1 || k == 2 || k == 4 || k == 8 || k == 16;
 }
 
@@ -172,6 +175,7 @@ int largest_fused_k(int kind, int64_t steps, int kmax) {
 
 int default_k(int kind, const sb_plan* P) {
     if (kind == KK_FUSED3D) return P->shape == SB_BOX ? 2 : 4;
+    if (kind == KK_FUSED2D) return 8;
     return 16;
 }
 
@@ -378,7 +382,8 @@ int make_tensor_maps(sb_plan* P) {
 template <typename T, bool BOX, int K, bool FMA>
 int launch_fused3d_k(sb_plan* P, int src_idx) {
     using TL = sb::F3Tile<T, K>;
-    auto kern = sb::fused3d_kernel<T, BOX, K, FMA>;
+    static const int minb = (int)env_double("SB200_3D_MINB", 2);
+    auto kern = minb == 2 ? sb::fused3d_kernel<T, BOX, K, FMA, 2> : sb::fused3d_kernel<T, BOX, K, FMA, 1>;
     const int smem = sb::f3_smem_bytes<T, K>();
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
@@ -438,6 +443,65 @@ int launch_fused3d(sb_plan* P, int src_idx, int k) {
     return launch_fused3d_b<T, false, FMA>(P, src_idx, k);
 }
 
+// ---------------------------------------------------------------- 2D
+
+template <typename T, bool BOX, int K, bool FMA>
+int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
+    using TL = sb::F2Tile<K>;
+    auto kern = sb::fused2d_kernel<T, BOX, K, FMA>;
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F2_WARPS * 32, 0));
+    occ = std::max(occ, 1);
+    sb::Fused2DParams<T> prm;
+    prm.src = src;
+    prm.dst = dst;
+    prm.origin = P->g.origin;
+    prm.sy = P->g.sy;
+    prm.ny = (int)P->dims[0];
+    prm.nx = (int)P->dims[1];
+    prm.row_lo = -(int)P->hlo;
+    prm.row_hi = (int)(P->dims[0] + P->hhi);
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    prm.tiles_x = (int)((P->dims[1] + TL::TXO - 1) / TL::TXO);
+    const int warps_max = P->num_sms * occ * sb::F2_WARPS;
+    const double per = env_double("SB200_2D_ITEMS_PER_WARP", 3.0);
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * warps_max / prm.tiles_x + 0.5)));
+    // keep segments long against the 2K-row warm-up
+    nseg = (int)std::min<int64_t>(nseg, std::max<int64_t>(1, P->dims[0] / (16 * K)));
+    prm.ly = (int)((P->dims[0] + nseg - 1) / nseg);
+    prm.nseg = (int)((P->dims[0] + prm.ly - 1) / prm.ly);
+    prm.items = prm.tiles_x * prm.nseg;
+    const int blocks = std::min(P->num_sms * occ, (prm.items + sb::F2_WARPS - 1) / sb::F2_WARPS);
+    prm.total_warps = blocks * sb::F2_WARPS;
+    prm.counter = P->d_counter;
+    for (int i = 0; i < 9; i++) prm.w[i] = T(0);
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[2 * i];
+        prm.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
+    }
+    kern<<<(unsigned)blocks, sb::F2_WARPS * 32, 0, P->stream>>>(prm);
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, bool BOX, bool FMA>
+int launch_fused2d_b(sb_plan* P, const T* src, T* dst, int k) {
+    switch (k) {
+        case 1: return launch_fused2d_k<T, BOX, 1, FMA>(P, src, dst);
+        case 2: return launch_fused2d_k<T, BOX, 2, FMA>(P, src, dst);
+        case 4: return launch_fused2d_k<T, BOX, 4, FMA>(P, src, dst);
+        case 8: return launch_fused2d_k<T, BOX, 8, FMA>(P, src, dst);
+        default: return fail(SB_ERR_ARG, "unsupported 2D fused depth %d", k);
+    }
+}
+
+template <typename T, bool FMA>
+int launch_fused2d(sb_plan* P, const T* src, T* dst, int k) {
+    if (P->shape == SB_BOX) return launch_fused2d_b<T, true, FMA>(P, src, dst, k);
+    return launch_fused2d_b<T, false, FMA>(P, src, dst, k);
+}
+
 // One launch advancing k levels from buf[cur] into buf[cur^1].
 template <typename T, bool FMA>
 int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
@@ -448,6 +512,8 @@ int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
         rc = launch_fused1d<T, FMA>(P, src, dst, k);
     } else if (P->kind == KK_FUSED3D) {
         rc = launch_fused3d<T, FMA>(P, P->cur, k);
+    } else if (P->kind == KK_FUSED2D) {
+        rc = launch_fused2d<T, FMA>(P, src, dst, k);
     } else {
         // generic: one level; on slab sides the valid range shrinks by r per level
         const int64_t n0 = P->dims[0];
@@ -508,6 +574,7 @@ int dispatch_run(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
 const char* kernel_name(const sb_plan* P) {
     if (P->kind == KK_FUSED1D) return "fused1d_kernel";
     if (P->kind == KK_FUSED3D) return "fused3d_kernel";
+    if (P->kind == KK_FUSED2D) return "fused2d_kernel";
     return "generic_step_kernel";
 }
 
@@ -592,7 +659,7 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
         if (!fused_k_ok(fk, P->k)) {
             delete P;
             return fail(SB_ERR_ARG, "fused depth k=%d unsupported by the %s kernel", prob->k,
-                        fk == KK_FUSED3D ? "3D (1..4)" : "1D (1, 2, 4, 8, 16)");
+                        fk == KK_FUSED3D ? "3D (1..4)" : fk == KK_FUSED2D ? "2D (1, 2, 4, 8)" : "1D (1, 2, 4, 8, 16)");
         }
     } else {
         P->kind = KK_GENERIC;

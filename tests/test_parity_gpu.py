@@ -231,3 +231,42 @@ def test_c5_full_size_fp32():
     want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 4)
     got = sweep(spec, box32, 4, arith="fma", k=2)
     assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+# --- fused 2D kernel (warp-independent y-streaming) -------------------------------
+
+@pytest.mark.parametrize("cfg", ["c3a", "c3b"])
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+@pytest.mark.parametrize("dims", [(3, 5), (40, 127), (301, 530)])
+def test_fused2d_every_depth_exact(cfg, k, dims):
+    spec = config_spec(cfg)
+    box = seeded_box(dims, 1, seed=sum(dims) + k)
+    T = 11
+    got = sweep(spec, box, T, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, T).tobytes()
+
+
+@pytest.mark.parametrize("k", [1, 4, 8])
+def test_fused2d_star_and_halo_zero(k):
+    spec = make_stencil_spec("2d5p")
+    box = seeded_box((129, 260), 1, seed=k, halo="zero")
+    got = sweep(spec, box, 13, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, 13).tobytes()
+
+
+def test_fused2d_fp32():
+    spec = config_spec("c3b")
+    box32 = seeded_box((200, 1000), 1, seed=4).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 24)
+    got = sweep(spec, box32, 24, arith="fma", kernel="fused", k=8)
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+@pytest.mark.parametrize("cfg", ["c3a", "c3b"])
+def test_c3_full_size_fma(cfg):
+    spec = config_spec(cfg)
+    box = seeded_box((16384, 16384), 1)
+    got = sweep(spec, box, 16, arith="fma", k=8)
+    want = oracle(spec, box, 16)
+    assert np_oracle.max_rel_error(got, want) <= FP64_TOL
