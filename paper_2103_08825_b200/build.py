@@ -14,14 +14,14 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libsb200.so")
-SOURCES = ["sb200.cu"]
+SOURCES = ["sb200.cu", "launch1d.cu", "launch2d.cu", "launch3d.cu"]  # compiled in parallel
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
 def _deps():
     out = []
     for name in os.listdir(CSRC):
-        if name.endswith((".cu", ".cuh", ".h")):
+        if name.endswith((".cu", ".cuh", ".h", ".hpp")):
             out.append(os.path.join(CSRC, name))
     out.append(os.path.join(os.path.dirname(PKG), "include", "sb200.h"))
     return out
@@ -38,19 +38,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
+    obj_dir = os.path.join(LIB_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
-    cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v", "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+    procs, objs = [], []
+    for src in SOURCES:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        objs.append(obj)
+        procs.append((src, subprocess.Popen([nvcc, *flags, "-c", os.path.join(CSRC, src), "-o", obj],
+                                            stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log = []
+    failed = False
+    for src, pr in procs:
+        out, err = pr.communicate()
+        log.append(err)
+        if pr.returncode != 0:
+            failed = True
+            sys.stderr.write(f"--- {src}\n" + out + err)
+    if failed:
+        raise RuntimeError("nvcc failed")
+    res = subprocess.run([nvcc, *ARCH, "-shared", "-o", LIB + ".tmp", *objs], capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode})")
+        raise RuntimeError(f"link failed ({res.returncode})")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(log))
     with open(os.path.join(LIB_DIR, "ptxas.log"), "w") as fh:
-        fh.write(res.stderr)
+        fh.write("".join(log))
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

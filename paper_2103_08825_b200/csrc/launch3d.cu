@@ -1,0 +1,116 @@
+// Launch unit of the fused 3D kernel (K3/K4): TMA descriptors, tile/segment work items.
+#include <cstdio>
+#include <cstdlib>
+
+#include "plan.hpp"
+#include "fused3d.cuh"
+
+namespace sbh {
+namespace {
+
+// ---------------------------------------------------------------- 3D
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// One TMA descriptor per device buffer: a 3D view (cols, rows, planes) of
+// the whole allocation; boxes of F3_PW x F3_PH x 1, OOB elements zero-filled.
+int make_tensor_maps_impl(sb_plan* P) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto encode = reinterpret_cast<EncodeTiledFn>(fn);
+    const int64_t rows = P->dims[1] + 2 * P->r;
+    const int64_t planes = P->hlo + P->dims[0] + P->hhi;
+    cuuint64_t dims[3] = {(cuuint64_t)P->px, (cuuint64_t)rows, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)(P->px * P->es), (cuuint64_t)(rows * P->px * P->es)};
+    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)sb::F3_PH, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = P->dtype == SB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    for (int b = 0; b < 2; b++) {
+        CUresult r = encode(&P->tmap[b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    return SB_OK;
+}
+
+template <typename T, bool BOX, int K, bool FMA>
+int launch_fused3d_k(sb_plan* P, int src_idx) {
+    using TL = sb::F3Tile<T, K>;
+    static const int minb = (int)env_double("SB200_3D_MINB", 2);
+    auto kern = minb == 2 ? sb::fused3d_kernel<T, BOX, K, FMA, 2> : sb::fused3d_kernel<T, BOX, K, FMA, 1>;
+    const int smem = sb::f3_smem_bytes<T, K>();
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3_THREADS, smem));
+    occ = std::max(occ, 1);
+    sb::Fused3DParams<T> prm;
+    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
+    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
+    prm.origin = P->g.origin;
+    prm.sz = P->g.sz;
+    prm.sy = P->g.sy;
+    prm.nz = (int)P->dims[0];
+    prm.ny = (int)P->dims[1];
+    prm.nx = (int)P->dims[2];
+    prm.ax = (int)(P->g.origin % P->g.sy);
+    prm.ry = P->r;
+    prm.hz = (int)P->hlo;
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    prm.ghost_lo = P->phys_lo ? 0 : (int)P->hlo;
+    prm.ghost_hi = P->phys_hi ? 0 : (int)P->hhi;
+    prm.tiles_x = (int)((P->dims[2] - TL::X0 + TL::TXO - 1) / TL::TXO);
+    prm.tiles_y = (int)((P->dims[1] + TL::TYO - 1) / TL::TYO);
+    const int ctas_max = P->num_sms * occ;
+    const int tiles = prm.tiles_x * prm.tiles_y;
+    const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", 6.0);
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(seg_env * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
+    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    prm.items = tiles * prm.nseg;
+    prm.total_ctas = std::min(ctas_max, prm.items);
+    prm.counter = P->d_counter;
+    for (int i = 0; i < 27; i++) prm.w[i] = T(0);
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[3 * i];
+        prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
+    }
+    kern<<<(unsigned)prm.total_ctas, sb::F3_THREADS, smem, P->stream>>>(P->tmap[src_idx], prm);
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, bool BOX, bool FMA>
+int launch_fused3d_b(sb_plan* P, int src_idx, int k) {
+    switch (k) {
+        case 1: return launch_fused3d_k<T, BOX, 1, FMA>(P, src_idx);
+        case 2: return launch_fused3d_k<T, BOX, 2, FMA>(P, src_idx);
+        case 3: return launch_fused3d_k<T, BOX, 3, FMA>(P, src_idx);
+        case 4: return launch_fused3d_k<T, BOX, 4, FMA>(P, src_idx);
+        default: return fail(SB_ERR_ARG, "unsupported 3D fused depth %d", k);
+    }
+}
+
+template <typename T, bool FMA>
+int launch_fused3d_t(sb_plan* P, int src_idx, int k) {
+    if (P->shape == SB_BOX) return launch_fused3d_b<T, true, FMA>(P, src_idx, k);
+    return launch_fused3d_b<T, false, FMA>(P, src_idx, k);
+}
+
+
+}  // namespace
+
+int launch_fused3d(sb_plan* P, int src_idx, int k) {
+    const bool fma = P->arith == SB_ARITH_FMA;
+    if (P->dtype == SB_F64) return fma ? launch_fused3d_t<double, true>(P, src_idx, k) : launch_fused3d_t<double, false>(P, src_idx, k);
+    return fma ? launch_fused3d_t<float, true>(P, src_idx, k) : launch_fused3d_t<float, false>(P, src_idx, k);
+}
+
+int make_tensor_maps(sb_plan* P) { return make_tensor_maps_impl(P); }
+
+}  // namespace sbh

@@ -1,0 +1,93 @@
+// Host-side plan state shared by the C-ABI unit (sb200.cu) and the kernel
+// launch units (launch1d.cu, launch2d.cu, launch3d.cu), compiled separately.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/sb200.h"
+#include "common.cuh"
+
+namespace sbh {
+
+int fail(int code, const char* fmt, ...);
+double env_double(const char* name, double dflt);   // development tuning knobs
+
+#define SB_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(SB_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+    } while (0)
+
+inline int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+constexpr int64_t kRightPad1D = 4096 + 1024;  // >= last-chunk overrun (< 32*Q) + lead + RK + Q
+constexpr int kMaxS1D = 4096;
+
+enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2, KK_FUSED3D = 3, KK_FUSED2D = 4 };
+
+struct Sched1D {
+    int K = 0;
+    int blocks = 0;
+    int nchunks = 0;   // interior chunks
+    int nedge = 0;     // boundary chunks (edge kernel)
+    void* d_chunks = nullptr;   // sb::Chunk1D[nchunks + nedge]
+};
+
+
+struct Chunk1DHost {
+    int64_t start;
+    int32_t S;
+    int32_t pad;
+};
+
+}  // namespace sbh
+
+struct sb_plan {
+    int d = 0, r = 0, shape = 0, nw = 0, dtype = 0, arith = 0, kreq = 0, kernel_req = 0;
+    int device = 0;
+    std::vector<int32_t> offsets;
+    std::vector<double> weights;
+    int64_t dims[3] = {1, 1, 1};  // interior, slowest first (first d used)
+    int64_t hlo = 0, hhi = 0;     // axis-0 halo/ghost depth on each side
+    bool phys_lo = true, phys_hi = true;
+    size_t es = 8;
+    sb::Geom g{};                 // canonical 3D geometry of the device buffers
+    int64_t px = 0;
+    size_t buf_elems = 0;
+    void* buf[2] = {nullptr, nullptr};
+    int cur = 0;
+    bool uploaded = false;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaStream_t side_stream = nullptr;            // boundary work forked from `stream`
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int64_t* d_lin = nullptr;
+    void* d_w = nullptr;
+    unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
+    std::vector<sbh::Sched1D> sched1d;
+    CUtensorMap tmap[2];                   // TMA descriptors of the two buffers (3D)
+    unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
+    int trace_n = 0;
+    int kind = sbh::KK_GENERIC;
+    int k = 1;
+    int num_sms = 148;
+    // host-box geometry
+    int64_t host_rows = 0, host_row_elems = 0, host_elems = 0;
+    int64_t host_dst_offset = 0;  // device element offset of host element 0
+};
+
+
+// Kernel-family launch entry points (one launch of k fused levels from
+// buf[src_idx] into buf[src_idx ^ 1]); each dispatches on dtype/arith.
+namespace sbh {
+int launch_fused1d(sb_plan* P, int src_idx, int k);
+int launch_fused2d(sb_plan* P, int src_idx, int k);
+int launch_fused3d(sb_plan* P, int src_idx, int k);
+int make_tensor_maps(sb_plan* P);
+}  // namespace sbh

@@ -18,14 +18,10 @@
 #include <string>
 #include <vector>
 
-#include "../../include/sb200.h"
-#include "common.cuh"
-#include "fused1d.cuh"
-#include "fused3d.cuh"
-#include "fused2d.cuh"
 #include "generic.cuh"
+#include "plan.hpp"
 
-namespace {
+namespace sbh {
 
 thread_local std::string g_err;
 
@@ -39,64 +35,16 @@ int fail(int code, const char* fmt, ...) {
     return code;
 }
 
-#define SB_CUDA(call)                                                                     \
-    do {                                                                                  \
-        cudaError_t e_ = (call);                                                          \
-        if (e_ != cudaSuccess)                                                            \
-            return fail(SB_ERR_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
-    } while (0)
+// Tuning knobs (development only; defaults are the measured best).
+double env_double(const char* name, double dflt) {
+    const char* v = getenv(name);
+    return v ? atof(v) : dflt;
+}
 
-int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
-constexpr int64_t kRightPad1D = 4096 + 1024;  // >= last-chunk overrun (< 32*Q) + lead + RK + Q
-constexpr int kMaxS1D = 4096;
+}  // namespace sbh
 
-enum KernelKind { KK_GENERIC = 1, KK_FUSED1D = 2, KK_FUSED3D = 3, KK_FUSED2D = 4 };
-
-struct Sched1D {
-    int K = 0;
-    int blocks = 0;
-    int nchunks = 0;   // interior chunks
-    int nedge = 0;     // boundary chunks (edge kernel)
-    sb::Chunk1D* d_chunks = nullptr;
-};
-
-}  // namespace
-
-struct sb_plan {
-    int d = 0, r = 0, shape = 0, nw = 0, dtype = 0, arith = 0, kreq = 0, kernel_req = 0;
-    int device = 0;
-    std::vector<int32_t> offsets;
-    std::vector<double> weights;
-    int64_t dims[3] = {1, 1, 1};  // interior, slowest first (first d used)
-    int64_t hlo = 0, hhi = 0;     // axis-0 halo/ghost depth on each side
-    bool phys_lo = true, phys_hi = true;
-    size_t es = 8;
-    sb::Geom g{};                 // canonical 3D geometry of the device buffers
-    int64_t px = 0;
-    size_t buf_elems = 0;
-    void* buf[2] = {nullptr, nullptr};
-    int cur = 0;
-    bool uploaded = false;
-    cudaStream_t own_stream = nullptr;
-    cudaStream_t stream = nullptr;
-    cudaStream_t side_stream = nullptr;            // boundary work forked from `stream`
-    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-    int64_t* d_lin = nullptr;
-    void* d_w = nullptr;
-    unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
-    std::vector<Sched1D> sched1d;
-    CUtensorMap tmap[2];                   // TMA descriptors of the two buffers (3D)
-    unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
-    int trace_n = 0;
-    int kind = KK_GENERIC;
-    int k = 1;
-    int num_sms = 148;
-    // host-box geometry
-    int64_t host_rows = 0, host_row_elems = 0, host_elems = 0;
-    int64_t host_dst_offset = 0;  // device element offset of host element 0
-};
+using namespace sbh;
 
 namespace {
 
@@ -196,312 +144,6 @@ int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
     return SB_OK;
 }
 
-// Tuning knobs (development only; defaults are the measured best).
-double env_double(const char* name, double dflt) {
-    const char* v = getenv(name);
-    return v ? atof(v) : dflt;
-}
-
-// Guided chunk schedule for the persistent 1D kernel.  Chunks are claimed in
-// list order: first one large chunk per warp (a fraction of the line), then
-// chunks shrinking with the remaining work so the tail is balanced, and last
-// the two minimum-size chunks touching the physical boundaries (they run the
-// slower EDGE path; a large one there was measured to hold a whole launch
-// back by ~50%).  S is a multiple of Q; the final chunk overruns n by
-// < 32*Q points (covered by the right pad).
-std::vector<sb::Chunk1D> guided_schedule_1d(int64_t n, int64_t warps, int Q, int64_t s_min,
-                                           bool phys_lo, bool phys_hi, int* n_edge) {
-    std::vector<sb::Chunk1D> main, edges;
-    auto mk = [&](int64_t start, int64_t S) {
-        sb::Chunk1D c;
-        c.start = start;
-        c.S = (int32_t)S;
-        c.pad = 0;
-        return c;
-    };
-    const int64_t edge = 32 * s_min;
-    const double frac = env_double("SB200_1D_FIRST_FRAC", 0.7);
-    const double div = env_double("SB200_1D_GUIDED_DIV", 2.0);
-    const int64_t fixed = (int64_t)env_double("SB200_1D_FIXED_S", 0);
-    if (n <= 3 * edge) {  // small line: minimum-size chunks, boundary ones on the edge path
-        for (int64_t pos = 0; pos < n; pos += edge) {
-            const bool e = (phys_lo && pos == 0) || (phys_hi && pos + edge >= n);
-            (e ? edges : main).push_back(mk(pos, s_min));
-        }
-    } else {
-        const int64_t lo = edge, hi = n - edge;
-        const int64_t first =
-            std::max<int64_t>(s_min, (int64_t)(frac * (double)(hi - lo) / (32.0 * warps)) / Q * Q);
-        int64_t pos = lo, issued = 0;
-        while (pos < hi) {
-            const int64_t rem = hi - pos;
-            int64_t S = issued < warps ? first : round_up((int64_t)(rem / (32 * warps * div)), Q);
-            if (fixed > 0) S = round_up(fixed, Q);
-            S = std::max<int64_t>(S, s_min);
-            S = std::min<int64_t>(S, kMaxS1D);
-            S = std::min<int64_t>(S, round_up((rem + 31) / 32, Q));
-            main.push_back(mk(pos, S));
-            pos += 32 * S;
-            issued++;
-        }
-        (phys_lo ? edges : main).push_back(mk(0, s_min));
-        if (pos < n) (phys_hi ? edges : main).push_back(mk(pos, round_up((n - pos + 31) / 32, Q)));
-    }
-    *n_edge = (int)edges.size();
-    main.insert(main.end(), edges.begin(), edges.end());
-    return main;
-}
-
-// ONE_PER_SMSP: one 4-warp CTA per SM (one warp per scheduler: no
-// arbitration between warps, up to 255 registers, deep cp.async ring).
-template <typename T, int R, int K, bool FMA, int MINB, int NST, bool ONE_PER_SMSP, bool DIAG = false>
-int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
-    using SH = sb::Fused1DShape<T, NST>;
-    auto kern = sb::fused1d_kernel<T, R, K, FMA, MINB, NST, DIAG>;
-    // one CTA per SM is enforced through the shared-memory request
-    const int smem = ONE_PER_SMSP ? std::max(SH::SMEM_BYTES, 120 * 1024) : SH::SMEM_BYTES;
-    Sched1D* sc = nullptr;
-    for (auto& e : P->sched1d)
-        if (e.K == K) sc = &e;
-    if (!sc) {
-        SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                     (int)cudaSharedmemCarveoutMaxShared));
-        int blocks_per_sm = 0;
-        SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, SH::WARPS * 32, smem));
-        blocks_per_sm = std::max(blocks_per_sm, 1);
-        Sched1D e;
-        e.K = K;
-        e.blocks = P->num_sms * blocks_per_sm;
-        const int64_t warps = (int64_t)e.blocks * SH::WARPS;
-        int n_edge = 0;
-        auto chunks = guided_schedule_1d(P->g.n[2], warps, SH::Q,
-                                         (int64_t)env_double("SB200_1D_SMIN", 12 * SH::Q),
-                                         P->phys_lo, P->phys_hi, &n_edge);
-        e.nchunks = (int)chunks.size() - n_edge;
-        e.nedge = n_edge;
-        auto ekern = sb::fused1d_edge_kernel<T, R, K, FMA, NST, DIAG>;
-        SB_CUDA(cudaFuncSetAttribute(ekern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T)));
-        SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Chunk1D) * chunks.size()));
-        SB_CUDA(cudaMemcpy(e.d_chunks, chunks.data(), sizeof(sb::Chunk1D) * chunks.size(),
-                           cudaMemcpyHostToDevice));
-        P->sched1d.push_back(e);
-        sc = &P->sched1d.back();
-    }
-    sb::Fused1DParams<T, R> prm;
-    prm.src = src + P->g.origin;
-    prm.dst = dst + P->g.origin;
-    prm.n = P->g.n[2];
-    prm.chunks = sc->d_chunks;
-    prm.nchunks = sc->nchunks;
-    prm.total_warps = sc->blocks * SH::WARPS;
-    prm.counter = P->d_counter;
-    prm.trace = nullptr;
-    if (getenv("SB200_TRACE")) {
-        if (!P->d_trace) SB_CUDA(cudaMalloc(&P->d_trace, sizeof(unsigned long long) * 4 * (1 << 20)));
-        if (sc->nchunks <= (1 << 20)) prm.trace = P->d_trace;
-        P->trace_n = sc->nchunks;
-    }
-    prm.phys_lo = P->phys_lo;
-    prm.phys_hi = P->phys_hi;
-    for (int i = 0; i < 2 * R + 1; i++) prm.w[i] = (T)P->weights[i];
-    if (sc->nedge > 0) {  // fork: boundary chunks on the side stream, concurrently
-        SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
-        SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
-        sb::fused1d_edge_kernel<T, R, K, FMA, NST, DIAG><<<(unsigned)sc->nedge, 32,
-            (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T), P->side_stream>>>(prm);
-        SB_CUDA(cudaGetLastError());
-        SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
-    }
-    kern<<<(unsigned)sc->blocks, SH::WARPS * 32, smem, P->stream>>>(prm);
-    SB_CUDA(cudaGetLastError());
-    if (sc->nedge > 0) SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));  // join
-    return SB_OK;
-}
-
-template <typename T, int R, bool FMA>
-int launch_fused1d_r(sb_plan* P, const T* src, T* dst, int k) {
-    static const int mode = (int)env_double("SB200_1D_MODE", 0);
-    switch (k) {
-        case 1: return launch_fused1d_k<T, R, 1, FMA, 1, 3, false>(P, src, dst);
-        case 2: return launch_fused1d_k<T, R, 2, FMA, 1, 3, false>(P, src, dst);
-        case 4: return launch_fused1d_k<T, R, 4, FMA, 1, 3, false>(P, src, dst);
-        case 8:
-            if (mode == 1) return launch_fused1d_k<T, R, 8, FMA, 1, 6, true>(P, src, dst);
-            if (mode == 2) return launch_fused1d_k<T, R, 8, FMA, 1, 3, false, true>(P, src, dst);
-            if (mode == 3) return launch_fused1d_k<T, R, 8, FMA, 1, 4, false>(P, src, dst);
-            if (mode == 4) return launch_fused1d_k<T, R, 8, FMA, 1, 5, false>(P, src, dst);
-            return launch_fused1d_k<T, R, 8, FMA, 1, 3, false>(P, src, dst);
-        case 16:
-            if (mode == 1) return launch_fused1d_k<T, R, 16, FMA, 1, 6, true>(P, src, dst);
-            if (mode == 2) return launch_fused1d_k<T, R, 16, FMA, 1, 3, false, true>(P, src, dst);
-            if (mode == 3) return launch_fused1d_k<T, R, 16, FMA, 1, 4, false>(P, src, dst);
-            if (mode == 4) return launch_fused1d_k<T, R, 16, FMA, 1, 5, false>(P, src, dst);
-            return launch_fused1d_k<T, R, 16, FMA, 1, 3, false>(P, src, dst);
-        default: return fail(SB_ERR_ARG, "unsupported fused depth %d", k);
-    }
-}
-
-template <typename T, bool FMA>
-int launch_fused1d(sb_plan* P, const T* src, T* dst, int k) {
-    if (P->r == 1) return launch_fused1d_r<T, 1, FMA>(P, src, dst, k);
-    return launch_fused1d_r<T, 2, FMA>(P, src, dst, k);
-}
-
-// ---------------------------------------------------------------- 3D
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-// One TMA descriptor per device buffer: a 3D view (cols, rows, planes) of
-// the whole allocation; boxes of F3_PW x F3_PH x 1, OOB elements zero-filled.
-int make_tensor_maps(sb_plan* P) {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    SB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    auto encode = reinterpret_cast<EncodeTiledFn>(fn);
-    const int64_t rows = P->dims[1] + 2 * P->r;
-    const int64_t planes = P->hlo + P->dims[0] + P->hhi;
-    cuuint64_t dims[3] = {(cuuint64_t)P->px, (cuuint64_t)rows, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)(P->px * P->es), (cuuint64_t)(rows * P->px * P->es)};
-    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)sb::F3_PH, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    const CUtensorMapDataType dt = P->dtype == SB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    for (int b = 0; b < 2; b++) {
-        CUresult r = encode(&P->tmap[b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    }
-    return SB_OK;
-}
-
-template <typename T, bool BOX, int K, bool FMA>
-int launch_fused3d_k(sb_plan* P, int src_idx) {
-    using TL = sb::F3Tile<T, K>;
-    static const int minb = (int)env_double("SB200_3D_MINB", 2);
-    auto kern = minb == 2 ? sb::fused3d_kernel<T, BOX, K, FMA, 2> : sb::fused3d_kernel<T, BOX, K, FMA, 1>;
-    const int smem = sb::f3_smem_bytes<T, K>();
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3_THREADS, smem));
-    occ = std::max(occ, 1);
-    sb::Fused3DParams<T> prm;
-    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
-    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
-    prm.origin = P->g.origin;
-    prm.sz = P->g.sz;
-    prm.sy = P->g.sy;
-    prm.nz = (int)P->dims[0];
-    prm.ny = (int)P->dims[1];
-    prm.nx = (int)P->dims[2];
-    prm.ax = (int)(P->g.origin % P->g.sy);
-    prm.ry = P->r;
-    prm.hz = (int)P->hlo;
-    prm.phys_lo = P->phys_lo;
-    prm.phys_hi = P->phys_hi;
-    prm.ghost_lo = P->phys_lo ? 0 : (int)P->hlo;
-    prm.ghost_hi = P->phys_hi ? 0 : (int)P->hhi;
-    prm.tiles_x = (int)((P->dims[2] - TL::X0 + TL::TXO - 1) / TL::TXO);
-    prm.tiles_y = (int)((P->dims[1] + TL::TYO - 1) / TL::TYO);
-    const int ctas_max = P->num_sms * occ;
-    const int tiles = prm.tiles_x * prm.tiles_y;
-    const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", 6.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(seg_env * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
-    prm.items = tiles * prm.nseg;
-    prm.total_ctas = std::min(ctas_max, prm.items);
-    prm.counter = P->d_counter;
-    for (int i = 0; i < 27; i++) prm.w[i] = T(0);
-    for (int i = 0; i < P->nw; i++) {
-        const int* o = &P->offsets[3 * i];
-        prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
-    }
-    kern<<<(unsigned)prm.total_ctas, sb::F3_THREADS, smem, P->stream>>>(P->tmap[src_idx], prm);
-    SB_CUDA(cudaGetLastError());
-    return SB_OK;
-}
-
-template <typename T, bool BOX, bool FMA>
-int launch_fused3d_b(sb_plan* P, int src_idx, int k) {
-    switch (k) {
-        case 1: return launch_fused3d_k<T, BOX, 1, FMA>(P, src_idx);
-        case 2: return launch_fused3d_k<T, BOX, 2, FMA>(P, src_idx);
-        case 3: return launch_fused3d_k<T, BOX, 3, FMA>(P, src_idx);
-        case 4: return launch_fused3d_k<T, BOX, 4, FMA>(P, src_idx);
-        default: return fail(SB_ERR_ARG, "unsupported 3D fused depth %d", k);
-    }
-}
-
-template <typename T, bool FMA>
-int launch_fused3d(sb_plan* P, int src_idx, int k) {
-    if (P->shape == SB_BOX) return launch_fused3d_b<T, true, FMA>(P, src_idx, k);
-    return launch_fused3d_b<T, false, FMA>(P, src_idx, k);
-}
-
-// ---------------------------------------------------------------- 2D
-
-template <typename T, bool BOX, int K, bool FMA>
-int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
-    using TL = sb::F2Tile<K>;
-    auto kern = sb::fused2d_kernel<T, BOX, K, FMA>;
-    int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F2_WARPS * 32, 0));
-    occ = std::max(occ, 1);
-    sb::Fused2DParams<T> prm;
-    prm.src = src;
-    prm.dst = dst;
-    prm.origin = P->g.origin;
-    prm.sy = P->g.sy;
-    prm.ny = (int)P->dims[0];
-    prm.nx = (int)P->dims[1];
-    prm.row_lo = -(int)P->hlo;
-    prm.row_hi = (int)(P->dims[0] + P->hhi);
-    prm.phys_lo = P->phys_lo;
-    prm.phys_hi = P->phys_hi;
-    prm.tiles_x = (int)((P->dims[1] + TL::TXO - 1) / TL::TXO);
-    const int warps_max = P->num_sms * occ * sb::F2_WARPS;
-    const double per = env_double("SB200_2D_ITEMS_PER_WARP", 3.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * warps_max / prm.tiles_x + 0.5)));
-    // keep segments long against the 2K-row warm-up
-    nseg = (int)std::min<int64_t>(nseg, std::max<int64_t>(1, P->dims[0] / (16 * K)));
-    prm.ly = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.ly - 1) / prm.ly);
-    prm.items = prm.tiles_x * prm.nseg;
-    const int blocks = std::min(P->num_sms * occ, (prm.items + sb::F2_WARPS - 1) / sb::F2_WARPS);
-    prm.total_warps = blocks * sb::F2_WARPS;
-    prm.counter = P->d_counter;
-    for (int i = 0; i < 9; i++) prm.w[i] = T(0);
-    for (int i = 0; i < P->nw; i++) {
-        const int* o = &P->offsets[2 * i];
-        prm.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
-    }
-    kern<<<(unsigned)blocks, sb::F2_WARPS * 32, 0, P->stream>>>(prm);
-    SB_CUDA(cudaGetLastError());
-    return SB_OK;
-}
-
-template <typename T, bool BOX, bool FMA>
-int launch_fused2d_b(sb_plan* P, const T* src, T* dst, int k) {
-    switch (k) {
-        case 1: return launch_fused2d_k<T, BOX, 1, FMA>(P, src, dst);
-        case 2: return launch_fused2d_k<T, BOX, 2, FMA>(P, src, dst);
-        case 4: return launch_fused2d_k<T, BOX, 4, FMA>(P, src, dst);
-        case 8: return launch_fused2d_k<T, BOX, 8, FMA>(P, src, dst);
-        default: return fail(SB_ERR_ARG, "unsupported 2D fused depth %d", k);
-    }
-}
-
-template <typename T, bool FMA>
-int launch_fused2d(sb_plan* P, const T* src, T* dst, int k) {
-    if (P->shape == SB_BOX) return launch_fused2d_b<T, true, FMA>(P, src, dst, k);
-    return launch_fused2d_b<T, false, FMA>(P, src, dst, k);
-}
-
 // One launch advancing k levels from buf[cur] into buf[cur^1].
 template <typename T, bool FMA>
 int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
@@ -509,11 +151,11 @@ int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
     T* dst = reinterpret_cast<T*>(P->buf[P->cur ^ 1]);
     int rc;
     if (P->kind == KK_FUSED1D) {
-        rc = launch_fused1d<T, FMA>(P, src, dst, k);
+        rc = launch_fused1d(P, P->cur, k);
     } else if (P->kind == KK_FUSED3D) {
-        rc = launch_fused3d<T, FMA>(P, P->cur, k);
+        rc = launch_fused3d(P, P->cur, k);
     } else if (P->kind == KK_FUSED2D) {
-        rc = launch_fused2d<T, FMA>(P, src, dst, k);
+        rc = launch_fused2d(P, P->cur, k);
     } else {
         // generic: one level; on slab sides the valid range shrinks by r per level
         const int64_t n0 = P->dims[0];
