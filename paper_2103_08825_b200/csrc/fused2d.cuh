@@ -173,7 +173,9 @@ fused2d_kernel(const Fused2DParams<T> P) {
 #pragma unroll
                         for (int j = 0; j < F2_VX; j++) {
                             if (y_out || ((out_mask >> j) & 1)) {
-                                const bool sh = y_shell && ((shell_mask >> j) & 1);
+                                // the y-shell test applies only to physical halo rows; ghost rows
+                                // (slab sides) are real grid rows whose x-halo cells are Dirichlet
+                                const bool sh = (!y_out || y_shell) && ((shell_mask >> j) & 1);
                                 done[j] = sh ? rowp[col[j]] : T(0);
                             }
                         }

@@ -1,0 +1,84 @@
+"""The reference-facing drop-in: METHODS-compatible step and jam_sweep-
+compatible sweep on GridBuffer objects (the package's NATURAL mirror of
+stencilbench.core.GridBuffer), checked the way the reference checks its own
+methods (tests/test_kernels.py:113-133, test_timejam.py:156-164)."""
+
+import numpy as np
+import pytest
+
+from conftest import seeded_box
+from oracle import c_oracle
+
+from paper_2103_08825_b200.core import GridError, canonical, config_spec, make_stencil_spec
+from paper_2103_08825_b200.grid import Layout, alloc_grid, alloc_like, compact_view
+from paper_2103_08825_b200.kernels import b200_step, b200_sweep, register
+
+
+class Counters:   # shape of stencilbench.kernels.Counters (kernels.py:43-69)
+    def __init__(self):
+        self.scalar_loads = self.scalar_stores = self.point_updates = 0
+
+
+def test_register_into_methods_registry():
+    methods = {"scalar": (Layout.NATURAL, None)}
+    register(methods, Layout.NATURAL)
+    assert methods["b200"] == (Layout.NATURAL, b200_step)
+
+
+def test_step_rejects_aliasing_and_ranges():
+    spec = make_stencil_spec("1d3p")
+    g = alloc_grid(spec, 16)
+    with pytest.raises(GridError, match="out-of-place"):
+        b200_step(g, g, spec)
+    with pytest.raises(GridError, match="ranges"):
+        b200_step(g, alloc_like(g), spec, ranges=[(0, 4)])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset,dims", [("1d3p", (1000,)), ("1d5p", (999,)), ("2d5p", (40, 70)),
+                                         ("2d9p", (41, 66)), ("3d7p", (9, 20, 33)), ("3d27p", (8, 21, 30))])
+def test_step_equals_oracle_step(preset, dims):
+    spec = make_stencil_spec(preset)
+    src = alloc_grid(spec, dims)
+    src.set_interior(np.random.default_rng(5).random(dims))
+    dst = alloc_like(src)
+    c = Counters()
+    b200_step(src, dst, spec, c)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(np.ascontiguousarray(compact_view(src)), spec.r, offs, ws, 1)
+    r = spec.r
+    assert np.array_equal(dst.natural_interior(), want[tuple(slice(r, s - r) for s in want.shape)])
+    assert c.point_updates == int(np.prod(dims))
+    assert not dst.data[..., :r].any()          # halo untouched (still zero)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,dims,k,T", [("c2", (4096,), 2, 100), ("c2", (4096,), 16, 100),
+                                          ("c4", (20, 30, 40), 4, 10), ("c3b", (100, 90), 8, 20)])
+def test_sweep_in_place_like_jam_sweep(cfg, dims, k, T):
+    spec = config_spec(cfg)
+    g = alloc_grid(spec, dims)
+    g.set_interior(np.random.default_rng(99).random(dims))
+    before = np.array(compact_view(g), copy=True)   # 1D views are contiguous: copy
+    buf = g.data
+    c = Counters()
+    b200_sweep(g, spec, k, T, c)
+    assert g.data is buf                      # advanced in place (test_timejam.py:148-153)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(before, spec.r, offs, ws, T)
+    r = spec.r
+    assert np.array_equal(g.natural_interior(), want[tuple(slice(r, s - r) for s in want.shape)])
+    assert c.point_updates == int(np.prod(dims)) * T
+
+
+@pytest.mark.gpu
+def test_reference_gridbuffer_if_importable():
+    ref = pytest.importorskip("stencilbench.core", reason="reference not present on this host")
+    from stencilbench.kernels import scalar_step
+    spec = ref.make_stencil_spec("2d9p")
+    a = ref.alloc_grid(spec, (33, 47), ref.Layout.NATURAL, 4)
+    a.set_interior(np.random.default_rng(1).random((33, 47)))
+    b, b2 = ref.alloc_like(a), ref.alloc_like(a)
+    scalar_step(a, b, spec)
+    b200_step(a, b2, spec)
+    assert np.array_equal(b.natural_interior(), b2.natural_interior())
