@@ -83,34 +83,49 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """nvidia-smi clocks/throttle sampling around the timed region.
+
+    Started before warm-up (nvidia-smi needs ~1 s to start); every sample is
+    time-stamped on arrival and summary() keeps those inside the timed window
+    [mark_start, mark_end] (the two nearest ones if the window is shorter
+    than the sampling period)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.sw_power_cap,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown")
+    NAMES = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
-        self.lines = []
+        self.samples = []          # (wall time, line)
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            deadline = time.time() + 5
+            while not self.samples and time.time() < deadline:
+                time.sleep(0.05)
         except (OSError, FileNotFoundError):
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.samples.append((time.time(), line.strip()))
 
-    def __exit__(self, *exc):
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -119,25 +134,26 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ("sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
-        for line in self.lines:
+        parsed = []
+        for t, line in self.samples:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                parsed.append((t, float(parts[0]), float(parts[1]), parts[3:7]))
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not parsed:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        loaded = [s for s in sm if s > 0.5 * (mx or s)] or sm
-        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        inside = [p for p in parsed if self.t0 is not None and self.t0 <= p[0] <= (self.t1 or p[0])]
+        window = "timed region"
+        if not inside:
+            mid = ((self.t0 or 0) + (self.t1 or 0)) / 2
+            inside = sorted(parsed, key=lambda p: abs(p[0] - mid))[:2]
+            window = "nearest to a timed region shorter than the sampling period"
+        reasons = sorted({nm for p in inside for nm, v in zip(self.NAMES, p[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(p[1] for p in inside), "sm_max_mhz": inside[-1][2],
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def dist_env():
@@ -251,40 +267,46 @@ def run_gpu_arm(args):
 
     if world > 1:
         from paper_2103_08825_b200.slab import SlabSweep
-        runner = SlabSweep(spec, (n,), rank=rank, world=world, k=k, arith=args.arith,
-                           device=device, group=None)
-        run_once = lambda: runner.run(T)              # noqa: E731
-        upload = lambda: runner.upload(host_in.numpy())   # noqa: E731
-        download = lambda: runner.download(host_out.numpy())  # noqa: E731
+        runner = SlabSweep(spec, (n * world,), rank=rank, world=world, k=k, arith=args.arith,
+                           device=device, stream_ptr=stream.cuda_stream)
         plan = runner.plan
+        host_in = torch.empty(plan.shape[0], dtype=torch.float64, pin_memory=True)
+        host_in.numpy()[:] = rng.random(plan.shape[0])
+        host_out = torch.empty_like(host_in, pin_memory=True)
+        run_once = lambda: runner.run(T)                      # noqa: E731
     else:
         plan = Plan(spec, (n,), k=k, arith=args.arith, device=device)
         plan.set_stream(stream.cuda_stream)
-        upload = lambda: plan.upload(host_in.numpy())       # noqa: E731
-        download = lambda: plan.download(host_out.numpy())  # noqa: E731
-        run_once = lambda: plan.launch(T)                   # noqa: E731
+        run_once = lambda: plan.launch(T)                     # noqa: E731
+    upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
+    download = lambda: plan.download(host_out.numpy())       # noqa: E731
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(device).start()
     upload()
     for _ in range(args.warmup):
         run_once()
     barrier()
 
-    launches_per_step = -(-T // k) if T % k == 0 else (T // k + bin(T % k).count("1"))
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(device) as clocks:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            run_once()
-        ev1.record(stream)
-        barrier()
+    kernels_before = plan.kernel_count()
+    barrier()
+    clocks.mark_start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        run_once()
+    ev1.record(stream)
+    barrier()
+    clocks.mark_end()
+    clocks.stop()
     ms = ev0.elapsed_time(ev1)
+    kernels = plan.kernel_count() - kernels_before            # this rank's launches, timed region
+    launches_per_step = (T + k - 1) // k                        # main-kernel launches per sweep
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -375,7 +397,9 @@ def run_gpu_arm(args):
                        "parallelism": f"slab{world}" if world > 1 else "single"},
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": kernels * world,
+            "gpu_launches_note": "all ranks; per sweep and rank: T/k main fused1d launches + "
+                                 "the same number of boundary (edge) kernels on a side stream",
             "clocks": clocks.summary(),
         }
         if sweep is not None:

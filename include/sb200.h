@@ -126,6 +126,9 @@ int sb_device_view(const sb_plan *plan, int which, void **base,
 /* Fused depth the plan will use per launch. */
 int sb_plan_k(const sb_plan *plan, int32_t *k);
 
+/* Kernels launched by this plan so far (all kernels: main, boundary, generic). */
+int sb_kernel_count(const sb_plan *plan, int64_t *count);
+
 const char *sb_last_error(void);
 int sb_abi_version(void);
 /* Number of CUDA devices visible (0 without a GPU; never fails). */

@@ -21,7 +21,7 @@ SB_KERNEL_AUTO, SB_KERNEL_GENERIC, SB_KERNEL_FUSED = 0, 1, 2
 #: every symbol include/sb200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_download", "sb_run", "sb_launch", "sb_set_stream", "sb_device_view",
-           "sb_plan_k", "sb_last_error", "sb_abi_version", "sb_device_count")
+           "sb_plan_k", "sb_kernel_count", "sb_last_error", "sb_abi_version", "sb_device_count")
 
 
 class SbProblem(ctypes.Structure):
@@ -71,12 +71,13 @@ def load():
     lib.sb_device_view.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int64), ctypes.c_int64 * 3]
     lib.sb_plan_k.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
+    lib.sb_kernel_count.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_last_error.argtypes = []
     lib.sb_abi_version.restype = ctypes.c_int
     lib.sb_device_count.restype = ctypes.c_int
     for name in ("sb_plan_create", "sb_host_elems", "sb_upload", "sb_download", "sb_run",
-                 "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k"):
+                 "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k", "sb_kernel_count"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -169,13 +169,16 @@ fused2d_kernel(const Fused2DParams<T> P) {
                     const bool y_out = (P.phys_lo && yc < 0) || (P.phys_hi && yc >= P.ny);
                     if (y_out || out_mask) {                  // Dirichlet halo, same at every level
                         const bool y_shell = yc >= -1 && yc <= P.ny;
+                        // rows outside the allocation (first completions of a ghost-side
+                        // segment) are garbage that never reaches a valid output: no load
+                        const bool y_alloc = yc >= P.row_lo && yc < P.row_hi;
                         const T* rowp = P.src + P.origin + (int64_t)yc * P.sy;
 #pragma unroll
                         for (int j = 0; j < F2_VX; j++) {
                             if (y_out || ((out_mask >> j) & 1)) {
                                 // the y-shell test applies only to physical halo rows; ghost rows
                                 // (slab sides) are real grid rows whose x-halo cells are Dirichlet
-                                const bool sh = (!y_out || y_shell) && ((shell_mask >> j) & 1);
+                                const bool sh = y_alloc && (!y_out || y_shell) && ((shell_mask >> j) & 1);
                                 done[j] = sh ? rowp[col[j]] : T(0);
                             }
                         }

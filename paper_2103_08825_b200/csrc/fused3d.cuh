@@ -60,6 +60,7 @@ struct Fused3DParams {
     int64_t origin, sz, sy;
     int nx, ny, nz;
     int ax, ry, hz;          // allocation coordinates of interior (0,0,0): col, row, plane
+    int hz_hi;               // planes allocated above the interior (halo or ghost)
     int phys_lo, phys_hi;    // z sides: physical halo (1) or ghost (0)
     int ghost_lo, ghost_hi;  // ghost depth on slab sides (0 on physical sides)
     int tiles_x, tiles_y, nseg, lz;
@@ -283,10 +284,14 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                         done[q >> 1][q & 1] = hv;
                     }
                 } else if (out_mask) {   // only threads owning points outside the x/y interior
+                    // planes below/above the allocation (first completions of a ghost-side
+                    // segment) are garbage that never reaches a valid output: no load
+                    const bool z_alloc = zc >= -P.hz && zc < P.nz + P.hz_hi;
 #pragma unroll
                     for (int q = 0; q < 8; q++)
                         if ((out_mask >> q) & 1)
-                            done[q >> 1][q & 1] = ((shell_mask >> q) & 1) ? P.src[hoff[q] + (int64_t)zc * P.sz] : T(0);
+                            done[q >> 1][q & 1] =
+                                (z_alloc && ((shell_mask >> q) & 1)) ? P.src[hoff[q] + (int64_t)zc * P.sz] : T(0);
                 }
                 if (l < K) {
                     T* o = sl + (l - 1) * PLANE;

@@ -119,6 +119,7 @@ int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
             (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T), P->side_stream>>>(prm);
         SB_CUDA(cudaGetLastError());
         SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+        P->kernels_launched++;
     }
     kern<<<(unsigned)sc->blocks, SH::WARPS * 32, smem, P->stream>>>(prm);
     SB_CUDA(cudaGetLastError());

@@ -60,6 +60,7 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
     prm.ax = (int)(P->g.origin % P->g.sy);
     prm.ry = P->r;
     prm.hz = (int)P->hlo;
+    prm.hz_hi = (int)P->hhi;
     prm.phys_lo = P->phys_lo;
     prm.phys_hi = P->phys_hi;
     prm.ghost_lo = P->phys_lo ? 0 : (int)P->hlo;

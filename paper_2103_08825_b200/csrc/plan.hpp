@@ -75,6 +75,7 @@ struct sb_plan {
     unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
     int trace_n = 0;
     int kind = sbh::KK_GENERIC;
+    int64_t kernels_launched = 0;   // every kernel launch (sb_kernel_count)
     int k = 1;
     int num_sms = 148;
     // host-box geometry

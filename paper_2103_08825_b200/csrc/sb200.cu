@@ -166,6 +166,7 @@ int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
     if (rc != SB_OK) return rc;
     P->cur ^= 1;
     ++*launches;
+    P->kernels_launched++;
     return SB_OK;
 }
 
@@ -489,6 +490,7 @@ int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
     SB_CUDA(cudaSetDevice(P->device));
     int64_t launches = 0;
     int k_used = 1;
+    const int64_t kernels_before = P->kernels_launched;
     SB_CUDA(cudaEventRecord(P->ev[0], P->stream));
     int rc = dispatch_run(P, steps, &launches, &k_used);
     if (rc != SB_OK) return rc;
@@ -508,7 +510,7 @@ int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
         SB_CUDA(cudaEventElapsedTime(&ms, P->ev[0], P->ev[1]));
         t->device_ms = ms;
         t->kernel_ms = ms;
-        t->launches = launches;
+        t->launches = P->kernels_launched - kernels_before;
         int64_t pts = 1;
         for (int a = 0; a < P->d; a++) pts *= P->dims[a];
         t->point_updates = pts * steps;
@@ -541,6 +543,12 @@ int sb_device_view(const sb_plan* P, int which, void** base, int64_t* origin, in
         strides[1] = P->g.sy;
         strides[2] = 1;
     }
+    return SB_OK;
+}
+
+int sb_kernel_count(const sb_plan* P, int64_t* count) {
+    if (!P || !count) return fail(SB_ERR_ARG, "NULL argument");
+    *count = P->kernels_launched;
     return SB_OK;
 }
 

@@ -147,6 +147,12 @@ class Plan:
     def set_stream(self, stream_ptr: int | None) -> None:
         _abi.check(self._lib.sb_set_stream(self._h, ctypes.c_void_p(stream_ptr or 0)))
 
+    def kernel_count(self) -> int:
+        """Kernels this plan has launched so far (main, boundary and generic)."""
+        c = ctypes.c_int64()
+        _abi.check(self._lib.sb_kernel_count(self._h, ctypes.byref(c)))
+        return int(c.value)
+
     def device_view(self, which: int = 0):
         """(base pointer, origin element offset, element strides) of a buffer."""
         base = ctypes.c_void_p()

@@ -168,7 +168,7 @@ def test_plan_reuse_and_timing():
         p.upload(box)
         t = p.run(20)
         assert t.point_updates == 100000 * 20
-        assert t.k_used == 8 and t.launches == 3          # 8 + 8 + 4
+        assert t.k_used == 8 and t.launches == 6          # (8 + 8 + 4) x (interior + boundary kernel)
         assert t.kernel_name == "fused1d_kernel"
         mid = p.download()
         p.run(20)
