@@ -323,9 +323,17 @@ def run_gpu_arm(args):
     fp_bound = peaks["fp64_tflops"] * 1e12 / flops_per_update / 1e9
     hbm_bound = peaks["hbm_gbs"] * 1e9 * k / ALG_BYTES_PER_POINT / 1e9
     per_gpu = value / world
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "r01_bench_kernel_traffic.json")
+    if os.path.exists(tpath) and world == 1:
+        with open(tpath) as fh:
+            tj = json.load(fh)
+        if f"<double, 2, {k}," in tj["kernel"]:          # same kernel instantiation as this run
+            traffic = tj["traffic_bytes"]
     roofline = {
         "bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": None,
+        "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic,
+        "traffic_source": "profiles/r01_bench_kernel_traffic.json (ncu --set full, one launch)",
         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": launch_ms,
         "peak_source": peaks["source"]["hbm"],
     }
