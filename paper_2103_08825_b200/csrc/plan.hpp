@@ -36,6 +36,8 @@ struct Sched1D {
     int nchunks = 0;   // interior chunks
     int nedge = 0;     // boundary chunks (edge kernel)
     void* d_chunks = nullptr;   // sb::Chunk1D[nchunks + nedge]
+    int64_t comp_lo = 0, comp_hi = 0;   // composed-stencil range (K < 0 entries)
+    std::vector<double> cw;             // composed weights
 };
 
 
@@ -76,6 +78,7 @@ struct sb_plan {
     int trace_n = 0;
     int kind = sbh::KK_GENERIC;
     int64_t kernels_launched = 0;   // every kernel launch (sb_kernel_count)
+    const char* last_kernel = nullptr;   // main kernel of the last launch (sb_timing.kernel_name)
     int k = 1;
     int num_sms = 148;
     // host-box geometry

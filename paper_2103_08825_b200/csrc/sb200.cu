@@ -215,6 +215,7 @@ int dispatch_run(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
 }
 
 const char* kernel_name(const sb_plan* P) {
+    if (P->last_kernel) return P->last_kernel;
     if (P->kind == KK_FUSED1D) return "fused1d_kernel";
     if (P->kind == KK_FUSED3D) return "fused3d_kernel";
     if (P->kind == KK_FUSED2D) return "fused2d_kernel";
