@@ -4,32 +4,43 @@
 // Replaces the reference's 2D paths -- scalar_step over the whole grid
 // (kernels.py:120-134) and the tessellated thread-pool runner
 // (tiling.py:372-417, whose tiles synchronise per stage) -- with a scheme
-// that needs no synchronisation at all:
+// that needs no block-level synchronisation at all:
 //  * one warp owns a strip of 32 x VX computed columns (VX per lane) and
-//    streams it along y; a work item is (strip, y segment), claimed from an
-//    atomic queue by persistent warps;
-//  * x-neighbours of a lane's VX values come from lanes +-1 by warp
-//    shuffles; at the strip edges they come from the loaded halo columns at
-//    level 0 and are garbage above it, so the valid strip shrinks by one
-//    column per side per level (overlapped tiles: output 32*VX - 2(K-1));
+//    streams it along y; a work item is (strip, y range), taken from a
+//    host-built guided schedule through one atomic (claims pipelined);
+//  * level-0 rows are staged by cp.async into a per-warp shared ring DEPTH
+//    rows deep (each lane's VX columns are one 32 B chunk: strips start so
+//    that it is 16 B aligned), the strip-edge halo columns by element copies;
+//  * x-neighbours of a lane's VX values come from lanes +-1 by warp shuffles;
+//    at the strip edges they come from the staged halo columns at level 0 and
+//    are garbage above it, so the valid strip shrinks by one column per side
+//    per level (overlapped strips: output 32*VX - 2(K-1) columns);
 //  * every level keeps two pending partial-sum rows per lane in registers
 //    (push form along y): an arriving level-(l-1) row a is folded into rows
 //    a+1 (dy=-1, first terms), a (dy=0) and a-1 (dy=+1, completing), so each
 //    output sums its terms in canonical (dy, dx) order -- bit-exact in EXACT
-//    mode (kernels.py:103-108);
-//  * level-0 rows are loaded straight into registers, DEPTH rows ahead.
-// Boundaries: as in the 3D kernel, emitted values outside the interior on a
-// physical side are replaced by the Dirichlet halo (global read), values
-// beyond the halo shell by 0; slab (ghost) sides along y compute normally.
+//    mode (kernels.py:103-108).
+// Boundaries: emitted values outside the interior on a physical side are
+// replaced by the Dirichlet halo (global read), beyond the halo shell by 0;
+// slab (ghost) sides along y compute normally.
 #pragma once
 #include "common.cuh"
+#include "fused1d.cuh"   // cp.async helpers, Vec16
 
 namespace sb {
 
 constexpr int F2_VX = 4;                 // columns per lane
 constexpr int F2_CW = 32 * F2_VX;        // computed strip width
 constexpr int F2_WARPS = 4;              // warps per CTA
-constexpr int F2_DEPTH = 4;              // level-0 rows in flight per warp
+constexpr int F2_DEPTH = 8;              // staged rows per warp
+constexpr int F2_ROWW = F2_CW + 8;       // shared row: 128 columns + edges + pad
+
+struct Item2D {
+    int32_t tix;     // strip index
+    int32_t ys0;     // output rows [ys0, ys1)
+    int32_t ys1;
+    int32_t pad;
+};
 
 template <typename T>
 struct Fused2DParams {
@@ -37,18 +48,33 @@ struct Fused2DParams {
     T* dst;
     int64_t origin, sy;      // element (y, x) at origin + y*sy + x
     int nx, ny;
-    int row_lo, row_hi;      // loadable rows [row_lo, row_hi) (halo or ghost included)
+    int row_lo, row_hi;      // allocated rows [row_lo, row_hi) (halo or ghost included)
     int phys_lo, phys_hi;    // y sides: physical halo (1) or ghost (0)
-    int tiles_x, nseg, ly, items;
+    int items;
+    const Item2D* sched;
     int total_warps;
     unsigned int* counter;   // [0] next item, [1] retired warps
     T w[9];                  // w[(dy+1)*3 + (dx+1)]; star uses 5 entries
 };
 
-template <int K>
+// Strip geometry: the computed strip origin xc = x0 - (K-1) must be 16 B
+// aligned (staged chunks), so the output width is a multiple of the 16 B
+// vector and strip 0 starts at X0 <= 0 with X0 == K-1 (mod VEC).
+template <typename T, int K>
 struct F2Tile {
-    static constexpr int TXO = F2_CW - 2 * (K - 1);
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int TXO = ((F2_CW - 2 * (K - 1)) / VEC) * VEC;
+    static constexpr int X0 = ((K - 1) % VEC == 0) ? 0 : ((K - 1) % VEC) - VEC;
 };
+
+template <typename T>   // one element (4 or 8 B), zero-filled when !valid
+__device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    if (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0));
+}
 
 template <typename T, bool BOX, bool FMA>
 __device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX], T (&P0)[F2_VX], T (&done)[F2_VX],
@@ -89,21 +115,30 @@ __device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX],
 template <typename T, bool BOX, int K, bool FMA>
 __global__ void __launch_bounds__(F2_WARPS * 32)
 fused2d_kernel(const Fused2DParams<T> P) {
-    using TL = F2Tile<K>;
-    const int lane = threadIdx.x & 31;
-    for (;;) {
-        unsigned item = 0;
-        if (lane == 0) item = atomicAdd(&P.counter[0], 1u);
-        item = __shfl_sync(0xffffffffu, item, 0);
-        if (item >= (unsigned)P.items) break;
-        const int tix = item % P.tiles_x, seg = item / P.tiles_x;
-        const int x0 = tix * TL::TXO;               // output strip origin
-        const int xc = x0 - (K - 1);                // computed strip origin
-        const int ys0 = seg * P.ly, ys1 = min(P.ny, ys0 + P.ly);
+    using TL = F2Tile<T, K>;
+    constexpr int VEC = 16 / (int)sizeof(T);
+    using V = typename Vec16<T>::type;
+    extern __shared__ __align__(16) unsigned char smem_f2[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* ring = reinterpret_cast<T*>(smem_f2) + warp * F2_DEPTH * F2_ROWW;
+    // shared row layout: [VEC-1] left edge, [VEC..VEC+CW) strip columns, [VEC+CW] right edge
+
+    auto claim_issue = [&]() -> unsigned {
+        unsigned id = 0;
+        if (lane == 0)
+            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(id) : "l"(&P.counter[0]) : "memory");
+        return id;
+    };
+    unsigned item = __shfl_sync(0xffffffffu, claim_issue(), 0);
+    while (item < (unsigned)P.items) {
+        const unsigned next_raw = claim_issue();        // resolved after this item
+        const Item2D it = P.sched[item];
+        const int x0 = TL::X0 + it.tix * TL::TXO;       // output strip origin
+        const int xc = x0 - (K - 1);                    // computed strip origin (16 B aligned)
+        const int ys0 = it.ys0, ys1 = it.ys1;
         const int p_first = ys0 - K;
         const int M = (ys1 - ys0) + 2 * K;
 
-        // per-lane column bookkeeping (fixed for the item)
         int col[F2_VX];
         unsigned out_mask = 0, shell_mask = 0, store_mask = 0;
 #pragma unroll
@@ -115,24 +150,29 @@ fused2d_kernel(const Fused2DParams<T> P) {
             const int cj = x - x0;
             store_mask |= (unsigned)(cj >= 0 && cj < TL::TXO && x >= 0 && x < P.nx) << j;
         }
+        const bool warp_out = __any_sync(0xffffffffu, out_mask != 0);   // strip touches the x halo
         const int ecol = lane == 0 ? xc - 1 : xc + F2_CW;   // strip-edge halo column (lanes 0, 31)
         const bool eload = (lane == 0 || lane == 31) && ecol >= -1 && ecol <= P.nx;
-        bool cload[F2_VX];
-#pragma unroll
-        for (int j = 0; j < F2_VX; j++) cload[j] = col[j] >= -1 && col[j] <= P.nx;
 
-        // level-0 rows in flight: ring of DEPTH rows of VX values + one edge value
-        T ring[F2_DEPTH][F2_VX + 1];
-        auto load_row = [&](int t, T (&dstv)[F2_VX + 1]) {
+        auto stage = [&](int t) {
+            T* row = ring + (t % F2_DEPTH) * F2_ROWW;
             const int y = p_first + t;
             const bool rok = t < M && y >= P.row_lo && y < P.row_hi;
-            const T* rowp = P.src + P.origin + (int64_t)y * P.sy;
+            const T* g = P.src + P.origin + (int64_t)y * P.sy;
 #pragma unroll
-            for (int j = 0; j < F2_VX; j++) dstv[j] = (rok && cload[j]) ? __ldg(rowp + col[j]) : T(0);
-            dstv[F2_VX] = (rok && eload) ? __ldg(rowp + ecol) : T(0);
+            for (int c = 0; c < F2_VX / VEC; c++) {
+                const int x = xc + F2_VX * lane + c * VEC;  // chunk start (16 B aligned)
+                const bool ok = rok && x >= -VEC && x <= P.nx;
+                cp_async16(row + VEC + F2_VX * lane + c * VEC, ok ? g + x : P.src, ok);
+            }
+            if (lane == 0 || lane == 31) {
+                const bool ok = rok && eload;
+                cp_async_elem<T>(row + (lane == 0 ? VEC - 1 : VEC + F2_CW), ok ? g + ecol : P.src, ok);
+            }
+            cp_async_commit();
         };
 #pragma unroll
-        for (int d = 0; d < F2_DEPTH; d++) load_row(d, ring[d]);
+        for (int t = 0; t < F2_DEPTH - 1; t++) stage(t);
 
         T Pm[K][F2_VX], P0[K][F2_VX];
 #pragma unroll
@@ -140,55 +180,59 @@ fused2d_kernel(const Fused2DParams<T> P) {
 #pragma unroll
             for (int j = 0; j < F2_VX; j++) Pm[l][j] = P0[l][j] = T(0);
 
-        for (int t0 = 0; t0 < M; t0 += F2_DEPTH) {
+        for (int t = 0; t < M; t++) {
+            cp_async_wait<F2_DEPTH - 2>();
+            __syncwarp();
+            const T* row = ring + (t % F2_DEPTH) * F2_ROWW;
+            T v[F2_VX];
 #pragma unroll
-            for (int d = 0; d < F2_DEPTH; d++) {
-                const int t = t0 + d;
-                if (t >= M) break;
-                T cur[F2_VX + 1];
+            for (int j = 0; j < F2_VX; j++) v[j] = row[VEC + F2_VX * lane + j];
+            T edge = lane == 0 ? row[VEC - 1] : row[VEC + F2_CW];
+            __syncwarp();                                   // slot t-1 fully read before restaging
+            stage(t + F2_DEPTH - 1);
+            const int a0 = p_first + t;
 #pragma unroll
-                for (int j = 0; j <= F2_VX; j++) cur[j] = ring[d][j];
-                load_row(t + F2_DEPTH, ring[d]);              // refill this slot, DEPTH ahead
-                const int a0 = p_first + t;
-                T v[F2_VX];
+            for (int l = 1; l <= K; l++) {
+                T u[F2_VX + 2];
+                const T left = __shfl_up_sync(0xffffffffu, v[F2_VX - 1], 1);
+                const T right = __shfl_down_sync(0xffffffffu, v[0], 1);
+                u[0] = lane == 0 ? edge : left;
+                u[F2_VX + 1] = lane == 31 ? edge : right;
 #pragma unroll
-                for (int j = 0; j < F2_VX; j++) v[j] = cur[j];
-                T edge = cur[F2_VX];
+                for (int j = 0; j < F2_VX; j++) u[j + 1] = v[j];
+                T done[F2_VX];
+                f2_push<T, BOX, FMA>(u, Pm[l - 1], P0[l - 1], done, P.w);
+                const int yc = a0 - l;                      // completed level-l row
+                const bool y_out = (P.phys_lo && yc < 0) || (P.phys_hi && yc >= P.ny);
+                if (y_out || warp_out) {                    // (warp-uniform) Dirichlet halo, same at every level
+                    const bool y_shell = yc >= -1 && yc <= P.ny;
+                    const bool y_alloc = yc >= P.row_lo && yc < P.row_hi;
+                    const T* rowp = P.src + P.origin + (int64_t)yc * P.sy;
 #pragma unroll
-                for (int l = 1; l <= K; l++) {
-                    T u[F2_VX + 2];
-                    const T left = __shfl_up_sync(0xffffffffu, v[F2_VX - 1], 1);
-                    const T right = __shfl_down_sync(0xffffffffu, v[0], 1);
-                    u[0] = lane == 0 ? edge : left;
-                    u[F2_VX + 1] = lane == 31 ? edge : right;
-#pragma unroll
-                    for (int j = 0; j < F2_VX; j++) u[j + 1] = v[j];
-                    T done[F2_VX];
-                    f2_push<T, BOX, FMA>(u, Pm[l - 1], P0[l - 1], done, P.w);
-                    const int yc = a0 - l;                    // completed level-l row
-                    const bool y_out = (P.phys_lo && yc < 0) || (P.phys_hi && yc >= P.ny);
-                    if (y_out || out_mask) {                  // Dirichlet halo, same at every level
-                        const bool y_shell = yc >= -1 && yc <= P.ny;
-                        // rows outside the allocation (first completions of a ghost-side
-                        // segment) are garbage that never reaches a valid output: no load
-                        const bool y_alloc = yc >= P.row_lo && yc < P.row_hi;
-                        const T* rowp = P.src + P.origin + (int64_t)yc * P.sy;
-#pragma unroll
-                        for (int j = 0; j < F2_VX; j++) {
-                            if (y_out || ((out_mask >> j) & 1)) {
-                                // the y-shell test applies only to physical halo rows; ghost rows
-                                // (slab sides) are real grid rows whose x-halo cells are Dirichlet
-                                const bool sh = y_alloc && (!y_out || y_shell) && ((shell_mask >> j) & 1);
-                                done[j] = sh ? rowp[col[j]] : T(0);
-                            }
+                    for (int j = 0; j < F2_VX; j++) {
+                        if (y_out || ((out_mask >> j) & 1)) {
+                            // the y-shell test applies only to physical halo rows; ghost rows
+                            // are real grid rows whose x-halo cells are Dirichlet
+                            const bool sh = y_alloc && (!y_out || y_shell) && ((shell_mask >> j) & 1);
+                            done[j] = sh ? rowp[col[j]] : T(0);
                         }
                     }
-                    if (l < K) {
+                }
+                if (l < K) {
 #pragma unroll
-                        for (int j = 0; j < F2_VX; j++) v[j] = done[j];
-                        edge = T(0);                          // beyond level 0 the strip edge is garbage
-                    } else if (yc >= ys0 && yc < ys1) {
-                        T* rowp = P.dst + P.origin + (int64_t)yc * P.sy;
+                    for (int j = 0; j < F2_VX; j++) v[j] = done[j];
+                    edge = T(0);                            // beyond level 0 the strip edge is garbage
+                } else if (yc >= ys0 && yc < ys1) {
+                    T* rowp = P.dst + P.origin + (int64_t)yc * P.sy;
+                    if (store_mask == (1u << F2_VX) - 1) {  // whole 16 B-aligned chunk: vector stores
+#pragma unroll
+                        for (int c = 0; c < F2_VX / VEC; c++) {
+                            V pack;
+#pragma unroll
+                            for (int e = 0; e < VEC; e++) reinterpret_cast<T*>(&pack)[e] = done[c * VEC + e];
+                            *reinterpret_cast<V*>(rowp + col[0] + c * VEC) = pack;
+                        }
+                    } else {
 #pragma unroll
                         for (int j = 0; j < F2_VX; j++)
                             if ((store_mask >> j) & 1) rowp[col[j]] = done[j];
@@ -196,6 +240,9 @@ fused2d_kernel(const Fused2DParams<T> P) {
                 }
             }
         }
+        cp_async_wait<0>();
+        __syncwarp();
+        item = __shfl_sync(0xffffffffu, next_raw, 0);
     }
     if (lane == 0) {
         const unsigned retired = atomicAdd(&P.counter[1], 1u);
@@ -205,5 +252,8 @@ fused2d_kernel(const Fused2DParams<T> P) {
         }
     }
 }
+
+template <typename T>
+constexpr int fused2d_smem_bytes() { return F2_WARPS * F2_DEPTH * F2_ROWW * (int)sizeof(T); }
 
 }  // namespace sb

@@ -10,13 +10,66 @@ namespace {
 
 // ---------------------------------------------------------------- 2D
 
+// Guided (strip, y-range) schedule: a first round of long ranges (about
+// FRAC of the work spread over all warps), then ranges shrinking with the
+// remaining work, never below MIN rows (each item re-computes a 2K-row
+// warm-up).  Items are claimed in list order.
+std::vector<sb::Item2D> guided_schedule_2d(int tiles_x, int64_t ny, int64_t warps, int K) {
+    const double frac = env_double("SB200_2D_FIRST_FRAC", 0.4);
+    const int64_t min_rows = std::max<int64_t>((int64_t)env_double("SB200_2D_MIN_ROWS", 24 * K), 8);
+    std::vector<sb::Item2D> out;
+    std::vector<int64_t> pos(tiles_x, 0);   // per-strip cursor
+    const int64_t total = (int64_t)tiles_x * ny;
+    const int64_t per_strip = std::max<int64_t>(1, (warps + tiles_x - 1) / tiles_x);
+    int64_t done = 0;
+    bool first = true;
+    while (done < total) {
+        // one round = about one item per warp: per_strip consecutive items on every strip
+        const int64_t rem = total - done;
+        int64_t len = first ? (int64_t)(frac * (double)total / (double)warps) : rem / (2 * warps);
+        len = std::max<int64_t>(len, min_rows);
+        first = false;
+        for (int64_t rep = 0; rep < per_strip; rep++) {
+            for (int t = 0; t < tiles_x; t++) {
+                if (pos[t] >= ny) continue;
+                const int64_t l = std::min<int64_t>(len, ny - pos[t]);
+                sb::Item2D it;
+                it.tix = t;
+                it.ys0 = (int32_t)pos[t];
+                it.ys1 = (int32_t)(pos[t] + l);
+                it.pad = 0;
+                out.push_back(it);
+                pos[t] += l;
+                done += l;
+            }
+        }
+    }
+    return out;
+}
+
 template <typename T, bool BOX, int K, bool FMA>
 int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
-    using TL = sb::F2Tile<K>;
+    using TL = sb::F2Tile<T, K>;
     auto kern = sb::fused2d_kernel<T, BOX, K, FMA>;
-    int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F2_WARPS * 32, 0));
-    occ = std::max(occ, 1);
+    const int smem = sb::fused2d_smem_bytes<T>();
+    Sched1D* sc = nullptr;
+    for (auto& e : P->sched1d)
+        if (e.K == 1000 + K) sc = &e;   // 2D schedules keyed by 1000 + K
+    if (!sc) {
+        SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int occ = 0;
+        SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F2_WARPS * 32, smem));
+        Sched1D e;
+        e.K = 1000 + K;
+        e.blocks = P->num_sms * std::max(occ, 1);
+        const int tiles_x = (int)((P->dims[1] - TL::X0 + TL::TXO - 1) / TL::TXO);
+        auto items = guided_schedule_2d(tiles_x, P->dims[0], (int64_t)e.blocks * sb::F2_WARPS, K);
+        e.nchunks = (int)items.size();
+        SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Item2D) * items.size()));
+        SB_CUDA(cudaMemcpy(e.d_chunks, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice));
+        P->sched1d.push_back(e);
+        sc = &P->sched1d.back();
+    }
     sb::Fused2DParams<T> prm;
     prm.src = src;
     prm.dst = dst;
@@ -28,16 +81,9 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     prm.row_hi = (int)(P->dims[0] + P->hhi);
     prm.phys_lo = P->phys_lo;
     prm.phys_hi = P->phys_hi;
-    prm.tiles_x = (int)((P->dims[1] + TL::TXO - 1) / TL::TXO);
-    const int warps_max = P->num_sms * occ * sb::F2_WARPS;
-    const double per = env_double("SB200_2D_ITEMS_PER_WARP", 3.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * warps_max / prm.tiles_x + 0.5)));
-    // keep segments long against the 2K-row warm-up
-    nseg = (int)std::min<int64_t>(nseg, std::max<int64_t>(1, P->dims[0] / (16 * K)));
-    prm.ly = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.ly - 1) / prm.ly);
-    prm.items = prm.tiles_x * prm.nseg;
-    const int blocks = std::min(P->num_sms * occ, (prm.items + sb::F2_WARPS - 1) / sb::F2_WARPS);
+    prm.items = sc->nchunks;
+    prm.sched = reinterpret_cast<const sb::Item2D*>(sc->d_chunks);
+    const int blocks = std::min(sc->blocks, (prm.items + sb::F2_WARPS - 1) / sb::F2_WARPS);
     prm.total_warps = blocks * sb::F2_WARPS;
     prm.counter = P->d_counter;
     for (int i = 0; i < 9; i++) prm.w[i] = T(0);
@@ -45,7 +91,8 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
         const int* o = &P->offsets[2 * i];
         prm.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
     }
-    kern<<<(unsigned)blocks, sb::F2_WARPS * 32, 0, P->stream>>>(prm);
+    P->last_kernel = "fused2d_kernel";
+    kern<<<(unsigned)blocks, sb::F2_WARPS * 32, smem, P->stream>>>(prm);
     SB_CUDA(cudaGetLastError());
     return SB_OK;
 }
