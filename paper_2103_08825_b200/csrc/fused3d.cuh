@@ -38,20 +38,26 @@
 namespace sb {
 
 constexpr int F3_CW = 64;        // computed region width (x)
-constexpr int F3_CH = 32;        // computed region height (y)
 constexpr int F3_PW = 68;        // shared plane width: ring + region + pad (16 B rows)
-constexpr int F3_PH = 34;        // shared plane height: ring + region + ring
-constexpr int F3_THREADS = 256;  // 32 (x) x 8 (y) threads, 2 x 4 points each
 constexpr int F3_NS0 = 4;        // TMA ring depth (level-0 planes)
 
-// Plane stride in elements: TMA destinations must be 128 B aligned.
-template <typename T>
-struct F3Plane {
-    static constexpr int ELEMS = ((F3_PW * F3_PH * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
-    static constexpr unsigned BOX_BYTES = F3_PW * F3_PH * sizeof(T);
+// CTA geometry: NTY thread rows of 32 threads, 2 x 4 points per thread, so the
+// computed region is 64 x (4*NTY) and the plane box 68 x (4*NTY + 2).
+template <int NTY>
+struct F3Geo {
+    static constexpr int THREADS = 32 * NTY;
+    static constexpr int CH = 4 * NTY;          // computed region height (y)
+    static constexpr int PH = CH + 2;           // shared plane height: ring + region + ring
 };
-template <typename T, int K>
-constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T>::ELEMS * (int)sizeof(T); }
+
+// Plane stride in elements: TMA destinations must be 128 B aligned.
+template <typename T, int NTY>
+struct F3Plane {
+    static constexpr int ELEMS = ((F3_PW * F3Geo<NTY>::PH * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
+    static constexpr unsigned BOX_BYTES = F3_PW * F3Geo<NTY>::PH * sizeof(T);
+};
+template <typename T, int K, int NTY>
+constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T, NTY>::ELEMS * (int)sizeof(T); }
 
 template <typename T>
 struct Fused3DParams {
@@ -74,11 +80,11 @@ struct Fused3DParams {
 // aligned (measured: an unaligned innermost coordinate traps with "illegal
 // instruction"), so the tile pitch is a multiple of the 16 B vector and the
 // tiles start at X0 <= 0 with X0 == K (mod VEC); columns x < 0 are not stored.
-template <typename T, int K>
+template <typename T, int K, int NTY>
 struct F3Tile {
     static constexpr int VEC = 16 / (int)sizeof(T);
     static constexpr int TXO = ((F3_CW - 2 * (K - 1)) / VEC) * VEC;   // output tile width
-    static constexpr int TYO = F3_CH - 2 * (K - 1);                   // output tile height
+    static constexpr int TYO = F3Geo<NTY>::CH - 2 * (K - 1);          // output tile height
     static constexpr int X0 = (K % VEC == 0) ? 0 : (K % VEC) - VEC;  // first tile's x origin
 };
 
@@ -187,12 +193,13 @@ __device__ __forceinline__ void f3_read(const T* plane, int tx, int ty, T (&v)[6
     }
 }
 
-template <typename T, bool BOX, int K, bool FMA, int MINB = 1>
-__global__ void __launch_bounds__(F3_THREADS, MINB)
+template <typename T, bool BOX, int K, bool FMA, int MINB, int NTY>
+__global__ void __launch_bounds__(F3Geo<NTY>::THREADS, MINB)
 fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
-    constexpr int PLANE = F3Plane<T>::ELEMS;
-    constexpr unsigned PLANE_BYTES = F3Plane<T>::BOX_BYTES;
-    using TL = F3Tile<T, K>;
+    constexpr int PLANE = F3Plane<T, NTY>::ELEMS;
+    constexpr unsigned PLANE_BYTES = F3Plane<T, NTY>::BOX_BYTES;
+    constexpr int F3_CH = F3Geo<NTY>::CH;
+    using TL = F3Tile<T, K, NTY>;
     extern __shared__ __align__(1024) unsigned char smem3d[];   // TMA destinations: 128 B aligned
     T* s0 = reinterpret_cast<T*>(smem3d);              // NS0 level-0 slots
     T* sl = s0 + F3_NS0 * PLANE;                       // levels 1..K-1, one plane each

@@ -15,8 +15,8 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // One TMA descriptor per device buffer: a 3D view (cols, rows, planes) of
-// the whole allocation; boxes of F3_PW x F3_PH x 1, OOB elements zero-filled.
-int make_tensor_maps_impl(sb_plan* P) {
+// the whole allocation; boxes of F3_PW x (region height + 2) x 1, OOB elements zero-filled.
+int make_tensor_maps_impl(sb_plan* P, int geo, int box_h) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     SB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -26,27 +26,32 @@ int make_tensor_maps_impl(sb_plan* P) {
     const int64_t planes = P->hlo + P->dims[0] + P->hhi;
     cuuint64_t dims[3] = {(cuuint64_t)P->px, (cuuint64_t)rows, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)(P->px * P->es), (cuuint64_t)(rows * P->px * P->es)};
-    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)sb::F3_PH, 1};
+    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)box_h, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUtensorMapDataType dt = P->dtype == SB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     for (int b = 0; b < 2; b++) {
-        CUresult r = encode(&P->tmap[b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CUresult r = encode(&P->tmap[geo][b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
+    P->tmap_ok[geo] = true;
     return SB_OK;
 }
 
-template <typename T, bool BOX, int K, bool FMA>
-int launch_fused3d_k(sb_plan* P, int src_idx) {
-    using TL = sb::F3Tile<T, K>;
-    static const int minb = (int)env_double("SB200_3D_MINB", 2);
-    auto kern = minb == 2 ? sb::fused3d_kernel<T, BOX, K, FMA, 2> : sb::fused3d_kernel<T, BOX, K, FMA, 1>;
-    const int smem = sb::f3_smem_bytes<T, K>();
+template <typename T, bool BOX, int K, bool FMA, int NTY, int MINB>
+int launch_fused3d_g(sb_plan* P, int src_idx) {
+    using TL = sb::F3Tile<T, K, NTY>;
+    constexpr int GEO = NTY == 8 ? 0 : 1;
+    if (!P->tmap_ok[GEO]) {
+        const int rc = make_tensor_maps_impl(P, GEO, sb::F3Geo<NTY>::PH);
+        if (rc != SB_OK) return rc;
+    }
+    auto kern = sb::fused3d_kernel<T, BOX, K, FMA, MINB, NTY>;
+    const int smem = sb::f3_smem_bytes<T, K, NTY>();
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3_THREADS, smem));
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3Geo<NTY>::THREADS, smem));
     occ = std::max(occ, 1);
     sb::Fused3DParams<T> prm;
     prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
@@ -81,9 +86,19 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
         const int* o = &P->offsets[3 * i];
         prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
     }
-    kern<<<(unsigned)prm.total_ctas, sb::F3_THREADS, smem, P->stream>>>(P->tmap[src_idx], prm);
+    P->last_kernel = "fused3d_kernel";
+    kern<<<(unsigned)prm.total_ctas, sb::F3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
     SB_CUDA(cudaGetLastError());
     return SB_OK;
+}
+
+template <typename T, bool BOX, int K, bool FMA>
+int launch_fused3d_k(sb_plan* P, int src_idx) {
+    // 1: 128-thread CTAs (64 x 16 regions, 4 per SM: barrier phases of different
+    // CTAs decorrelate; measured better at K <= 2), 0: 256-thread CTAs (64 x 32)
+    static const int geo = (int)env_double("SB200_3D_GEO", -1);
+    if (geo == 1 || (geo < 0 && K <= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 4>(P, src_idx);
+    return launch_fused3d_g<T, BOX, K, FMA, 8, 2>(P, src_idx);
 }
 
 template <typename T, bool BOX, bool FMA>
@@ -112,6 +127,6 @@ int launch_fused3d(sb_plan* P, int src_idx, int k) {
     return fma ? launch_fused3d_t<float, true>(P, src_idx, k) : launch_fused3d_t<float, false>(P, src_idx, k);
 }
 
-int make_tensor_maps(sb_plan* P) { return make_tensor_maps_impl(P); }
+int make_tensor_maps(sb_plan* P, int geo, int box_h) { return make_tensor_maps_impl(P, geo, box_h); }
 
 }  // namespace sbh

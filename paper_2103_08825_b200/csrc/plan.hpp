@@ -73,7 +73,8 @@ struct sb_plan {
     void* d_w = nullptr;
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<sbh::Sched1D> sched1d;
-    CUtensorMap tmap[2];                   // TMA descriptors of the two buffers (3D)
+    CUtensorMap tmap[2][2];                // TMA descriptors [geometry][buffer] (3D)
+    bool tmap_ok[2] = {false, false};
     unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
     int trace_n = 0;
     int kind = sbh::KK_GENERIC;
@@ -93,5 +94,5 @@ namespace sbh {
 int launch_fused1d(sb_plan* P, int src_idx, int k);
 int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
-int make_tensor_maps(sb_plan* P);
+int make_tensor_maps(sb_plan* P, int geo, int box_h);
 }  // namespace sbh

@@ -421,13 +421,6 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
         std::vector<float> wf(P->weights.begin(), P->weights.end());
         SB_CUDA_P(cudaMemcpy(P->d_w, wf.data(), 4 * P->nw, cudaMemcpyHostToDevice));
     }
-    if (P->kind == KK_FUSED3D) {
-        const int trc = make_tensor_maps(P);
-        if (trc != SB_OK) {
-            sb_plan_destroy(P);
-            return trc;
-        }
-    }
     SB_CUDA_P(cudaStreamSynchronize(P->stream));
 #undef SB_CUDA_P
     *out = P;
