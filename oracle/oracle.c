@@ -22,7 +22,7 @@
  * Storage convention (the C-ABI's host convention, include/sb200.h): a
  * compact C-order box of shape (n_0+2r, ..., n_{d-1}+2r) holding interior
  * plus an r-deep Dirichlet halo that is read and never written.
- * Parallelised over rows with OpenMP; results do not depend on the thread
+ * Parallelised over (row, x-chunk) tasks with OpenMP; results do not depend on the thread
  * count (each point's sum is computed by one thread in canonical order).
  */
 #include <stdint.h>
@@ -66,26 +66,33 @@ static int64_t *lin_offsets(int d, int nw, const int32_t *offsets, const geom3 *
     return lin;
 }
 
+/* Work is split into (row, x-chunk) tasks so 1D lines use every thread too;
+ * each point is still computed by one thread in canonical order. */
+#define OR_CHUNK 2048   /* 16 KB of `out`: stays in L1 across the per-offset passes */
 #define DEFINE_STEP(NAME, T)                                                       \
 __attribute__((target_clones("avx2", "default")))                                  \
 static void NAME(const T *src, T *dst, const geom3 *g, int nw,                     \
                  const int64_t *lin, const T *w, int nthreads) {                   \
     const int64_t nz = g->n[0], ny = g->n[1], nx = g->n[2];                        \
     const int64_t base0 = g->h[0] * g->s[0] + g->h[1] * g->s[1] + g->h[2];         \
+    const int64_t nch = (nx + OR_CHUNK - 1) / OR_CHUNK;                            \
+    const int64_t tasks = nz * ny * nch;                                           \
     (void)nthreads;                                                                \
-    _Pragma("omp parallel for collapse(2) schedule(static) num_threads(nthreads)") \
-    for (int64_t z = 0; z < nz; z++) {                                             \
-        for (int64_t y = 0; y < ny; y++) {                                         \
-            const int64_t row = base0 + z * g->s[0] + y * g->s[1];                 \
-            T *out = dst + row;                                                    \
-            for (int64_t x = 0; x < nx; x++) out[x] = (T)0;                        \
-            for (int i = 0; i < nw; i++) {                                         \
-                const T wi = w[i];                                                 \
-                const T *in = src + row + lin[i];                                  \
-                for (int64_t x = 0; x < nx; x++) {                                 \
-                    T prod = wi * in[x];                                           \
-                    out[x] = out[x] + prod;                                        \
-                }                                                                  \
+    _Pragma("omp parallel for schedule(static) num_threads(nthreads)")             \
+    for (int64_t task = 0; task < tasks; task++) {                                 \
+        const int64_t c = task % nch, zy = task / nch;                             \
+        const int64_t z = zy / ny, y = zy % ny;                                    \
+        const int64_t x0 = c * OR_CHUNK;                                           \
+        const int64_t x1 = x0 + OR_CHUNK < nx ? x0 + OR_CHUNK : nx;                \
+        const int64_t row = base0 + z * g->s[0] + y * g->s[1];                     \
+        T *out = dst + row;                                                        \
+        for (int64_t x = x0; x < x1; x++) out[x] = (T)0;                           \
+        for (int i = 0; i < nw; i++) {                                             \
+            const T wi = w[i];                                                     \
+            const T *in = src + row + lin[i];                                      \
+            for (int64_t x = x0; x < x1; x++) {                                    \
+                T prod = wi * in[x];                                               \
+                out[x] = out[x] + prod;                                            \
             }                                                                      \
         }                                                                          \
     }                                                                              \
