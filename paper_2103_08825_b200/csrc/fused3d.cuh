@@ -193,6 +193,65 @@ __device__ __forceinline__ void f3_read(const T* plane, int tx, int ty, T (&v)[6
     }
 }
 
+// Row-streaming form of f3_read + f3_push: the arriving plane is read one row
+// (4 values) at a time and folded into the point-rows it touches, so only 4
+// plane values are live instead of 24.  Rows arrive in increasing dy and dx
+// ascends within a row, so each accumulator still receives its terms in
+// canonical (dy, dx) order within its dz group.
+template <typename T, bool BOX, bool FMA>
+__device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (&Pm)[4][2], T (&P0)[4][2],
+                                             T (&done)[4][2], const T* w) {
+    T nx[4][2];
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+        T u[4];
+        const T* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
+        if (sizeof(T) == 8) {
+            const double2 a = *reinterpret_cast<const double2*>(row);
+            const double2 b = *reinterpret_cast<const double2*>(row + 2);
+            u[0] = (T)a.x; u[1] = (T)a.y; u[2] = (T)b.x; u[3] = (T)b.y;
+        } else {
+            const float2 a = *reinterpret_cast<const float2*>(row);
+            const float2 b = *reinterpret_cast<const float2*>(row + 2);
+            u[0] = (T)a.x; u[1] = (T)a.y; u[2] = (T)b.x; u[3] = (T)b.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int dy = r - i - 1;                   // this row's dy for point-row i
+            if (dy < -1 || dy > 1) continue;
+#pragma unroll
+            for (int dx = -1; dx <= 1; dx++) {
+                const int q = (dy + 1) * 3 + (dx + 1);
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const T x = u[j + 1 + dx];
+                    if (BOX) {
+                        Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[18 + q], x);   // dz=+1: completes a-1
+                        P0[i][j] = acc_term<T, FMA>(P0[i][j], w[9 + q], x);    // dz= 0
+                        nx[i][j] = q == 0 ? acc_first<T, FMA>(w[0], x)         // dz=-1: starts a+1
+                                          : acc_term<T, FMA>(nx[i][j], w[q], x);
+                    } else {
+                        if (q == 4) {
+                            Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[22], x);   // (1,0,0)
+                            nx[i][j] = acc_first<T, FMA>(w[4], x);             // (-1,0,0)
+                        }
+                        if (q == 1 || q == 3 || q == 4 || q == 5 || q == 7)    // (0,dy,dx) of the star
+                            P0[i][j] = acc_term<T, FMA>(P0[i][j], w[9 + q], x);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            done[i][j] = Pm[i][j];
+            Pm[i][j] = P0[i][j];
+            P0[i][j] = nx[i][j];
+        }
+}
+
 template <typename T, bool BOX, int K, bool FMA, int MINB, int NTY>
 __global__ void __launch_bounds__(F3Geo<NTY>::THREADS, MINB)
 fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
@@ -276,10 +335,8 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
 #pragma unroll
             for (int l = 1; l <= K; l++) {
                 const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE : sl + (l - 2) * PLANE;
-                T v[6][4];
-                f3_read<T>(in, tx, ty, v);
                 T done[4][2];
-                f3_push<T, BOX, FMA>(v, Pm[l - 1], P0[l - 1], done, P.w);
+                f3_push_rows<T, BOX, FMA>(in, tx, ty, Pm[l - 1], P0[l - 1], done, P.w);
                 const int zc = a0 - l;    // completed level-l plane
                 const bool z_out = (P.phys_lo && zc < 0) || (P.phys_hi && zc >= P.nz);
                 if (z_out) {   // uniform: a physical halo plane, every value is Dirichlet
