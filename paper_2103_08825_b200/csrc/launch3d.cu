@@ -75,7 +75,9 @@ int launch_fused3d_g(sb_plan* P, int src_idx) {
     prm.tiles_y = (int)((P->dims[1] + TL::TYO - 1) / TL::TYO);
     const int ctas_max = P->num_sms * occ;
     const int tiles = prm.tiles_x * prm.tiles_y;
-    const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", 6.0);
+    // small uniform z-segments balance best (measured: k=2 10-16 per CTA, k=1 ~32);
+    // each item re-computes a 2K-plane warm-up, so not smaller
+    const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", K == 1 ? 32.0 : 12.0);
     int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(seg_env * ctas_max / tiles + 0.5)));
     prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
     prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
