@@ -3,7 +3,8 @@
 
 Workload (N=1): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
 N=2^26 interior points, T=1000 steps, coefficients (1/16, 1/4, 3/8, 1/4,
-1/16), fixed halo, fusion depth k swept over {1,2,4,8,16} (default k=16, the fastest).
+1/16), fixed halo, fused depth k (default: the plan's -- 32 in FMA mode, the
+composed-stencil kernel; ``--sweep-k`` also times k in {1,2,4,8,16,32}).
 One bench "step" = one full sweep (T=1000 time steps over the whole grid).
 At N>1 GPUs the same workload is weak-scaled: each rank owns a 2^26-point
 slab of a 2^26*N-point line, with an r*k-deep ghost exchange every launch.
@@ -49,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
-    ap.add_argument("--k", type=int, default=16)
+    ap.add_argument("--k", type=int, default=0, help="fusion depth (0: the plan default, 32 for C2 in FMA mode)")
     ap.add_argument("--arith", default="fma", choices=["fma", "exact"])
     ap.add_argument("--sweep-k", action="store_true", help="also time k in {1,2,4,8,16}")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -267,6 +268,7 @@ def run_gpu_arm(args):
 
     if world > 1:
         from paper_2103_08825_b200.slab import SlabSweep
+        k = k or (32 if args.arith == "fma" else 16)
         runner = SlabSweep(spec, (n * world,), rank=rank, world=world, k=k, arith=args.arith,
                            device=device, stream_ptr=stream.cuda_stream)
         plan = runner.plan
@@ -276,6 +278,7 @@ def run_gpu_arm(args):
         run_once = lambda: runner.run(T)                      # noqa: E731
     else:
         plan = Plan(spec, (n,), k=k, arith=args.arith, device=device)
+        k = plan.k
         plan.set_stream(stream.cuda_stream)
         run_once = lambda: plan.launch(T)                     # noqa: E731
     upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
@@ -314,39 +317,55 @@ def run_gpu_arm(args):
     ms_per_step = ms / args.steps
     value = n * world * T / (ms_per_step * 1e-3) / 1e9
 
-    # kernel share: one main kernel; its average launch duration over the timed region
+    # Dominant kernel: one main kernel per launch of k steps, average launch
+    # duration over the timed region (edge work overlaps it on a side stream).
     launch_ms = ms_per_step / launches_per_step
     peaks = measured_peaks()
-    alg_bytes = ALG_BYTES_PER_POINT * n
-    achieved_gbs = alg_bytes / (launch_ms * 1e-3) / 1e9
-    flops_per_update = 2 * len(spec.weights) - 1
+    per_gpu = value / world
+    flops_per_update = 2 * len(spec.weights) - 1            # BASELINE's F = 2|W| - 1
     fp_bound = peaks["fp64_tflops"] * 1e12 / flops_per_update / 1e9
     hbm_bound = peaks["hbm_gbs"] * 1e9 * k / ALG_BYTES_PER_POINT / 1e9
-    per_gpu = value / world
+    binding = "hbm" if hbm_bound < fp_bound else "fp64"
+    composed = args.arith == "fma" and k >= 16               # compose1d_kernel path (launch1d.cu)
+    kernel_name = f"compose1d_kernel<double, {spec.r * k}>" if composed else f"fused1d_kernel (K={k})"
+    # algorithmic work per launch of k steps: 16 B per point (read + write once),
+    # F flops per point update
+    alg_bytes = ALG_BYTES_PER_POINT * n
+    alg_flops = flops_per_update * n * k
+    achieved_gbs = alg_bytes / (launch_ms * 1e-3) / 1e9
+    achieved_tflops = per_gpu * 1e9 * flops_per_update / 1e12   # = alg_flops / launch time
     traffic = None
     tpath = os.path.join(REPO, "profiles", "r01_bench_kernel_traffic.json")
     if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             tj = json.load(fh)
-        if (k == 16 and args.arith == "fma" and "compose1d_kernel<double, 32>" in tj["kernel"]):  # same kernel
+        if composed and kernel_name in tj["kernel"]:           # the same kernel instantiation
             traffic = tj["traffic_bytes"]
+    hbm_view = {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved_gbs / peaks["hbm_gbs"], "alg_bytes_per_launch": alg_bytes,
+                "peak_source": peaks["source"]["hbm"]}
+    fp_view = {"achieved": achieved_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+               "frac": achieved_tflops / peaks["fp64_tflops"], "alg_flops_per_launch": alg_flops,
+               "peak_source": peaks["source"]["fp64"]}
+    main = fp_view if binding == "fp64" else hbm_view
     roofline = {
-        "bound": "hbm", "achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-        "frac": achieved_gbs / peaks["hbm_gbs"], "traffic": traffic,
-        "traffic_source": "profiles/r01_bench_kernel_traffic.json (ncu --set full, one launch)",
-        "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": launch_ms,
-        "peak_source": peaks["source"]["hbm"],
+        "bound": binding, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
+        "frac": main["frac"], "traffic": traffic,
+        "traffic_source": "profiles/r01_bench_kernel_traffic.json (ncu --set full, one launch: "
+                          "dram__bytes_read.sum + dram__bytes_write.sum)",
+        "kernel": kernel_name, "avg_launch_ms": launch_ms,
+        "note": "bound = the lower of the HBM roofline (16 B/point/launch) and the FP64 roofline "
+                "(F flops/update); 'fp64' is the CUDA-core FP64 pipe (a stencil is not a "
+                "tensor-core contraction)",
+        "hbm": hbm_view, "fp64": fp_view,
     }
     stencil_roofline = {
         "k": k, "hbm_bound_gstencil": hbm_bound, "fp64_bound_gstencil": fp_bound,
-        "fp64_peak_tflops": peaks["fp64_tflops"], "fp64_peak_source": peaks["source"]["fp64"],
-        "binding": "hbm" if hbm_bound < fp_bound else "fp64",
-        "achieved_gstencil_per_gpu": per_gpu,
+        "binding": binding, "achieved_gstencil_per_gpu": per_gpu,
         "frac": per_gpu / min(hbm_bound, fp_bound),
-        "fp64_tflops_achieved": per_gpu * 1e9 * flops_per_update / 1e12,
         "note": "frac uses BASELINE's algorithmic F = 2|W|-1 flops per update",
     }
-    if args.arith == "fma" and k == 16:
+    if composed:
         # composed-stencil path: (2RK+1) FMAs per point per launch of k steps
         fma_per_update = (2 * spec.r * k + 1) / k
         fma_rate = per_gpu * 1e9 * fma_per_update
@@ -380,7 +399,7 @@ def run_gpu_arm(args):
     sweep = None
     if args.sweep_k and world == 1:
         sweep = {}
-        for kk in (1, 2, 4, 8, 16):
+        for kk in (1, 2, 4, 8, 16, 32):
             with Plan(spec, (n,), k=kk, arith=args.arith, device=device) as p:
                 p.upload(host_in.numpy())
                 p.run(T // 4)
@@ -417,8 +436,8 @@ def run_gpu_arm(args):
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels * world,
-            "gpu_launches_note": "all ranks; per sweep and rank: T/k main fused1d launches + "
-                                 "the same number of boundary (edge) kernels on a side stream",
+            "gpu_launches_note": "all ranks; per sweep and rank: ceil(T/k) main launches + "
+                                 "the same number of boundary kernels on a side stream",
             "clocks": clocks.summary(),
         }
         if sweep is not None:

@@ -129,9 +129,10 @@ int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
     return SB_OK;
 }
 
-// Composed-stencil path (FMA mode, K >= 2): exact level-by-level edge kernel
-// for the chunks within reach of a physical boundary (side stream) and the
-// composed (2RK+1)-tap kernel for everything between (main stream).
+// Composed-stencil path (FMA mode): the composed (2RK+1)-tap kernel for every
+// output at least RK from a physical boundary (main stream) and, on the side
+// stream, one exact level-by-level window CTA per physical side for the RK
+// outputs next to it (their dependency cone reaches the Dirichlet halo).
 std::vector<double> composed_weights(const std::vector<double>& w, int K) {
     std::vector<long double> c(1, 1.0L);
     for (int step = 0; step < K; step++) {
@@ -146,72 +147,41 @@ std::vector<double> composed_weights(const std::vector<double>& w, int K) {
 template <typename T, int R, int K>
 int launch_compose1d_k(sb_plan* P, const T* src, T* dst) {
     constexpr int HALF = R * K;
-    using SH = sb::Fused1DShape<T, 3>;
-    constexpr int VEC = SH::VEC;
+    static_assert(2 * HALF + 1 <= sb::C1_MAXTAPS, "composed depth too large");
     const int64_t n = P->g.n[2];
-    const int64_t s_min = (int64_t)env_double("SB200_1D_SMIN", 12 * SH::Q);
-    const int64_t edge = 32 * s_min;
     Sched1D* sc = nullptr;
     for (auto& e : P->sched1d)
         if (e.K == -K) sc = &e;   // composed schedules keyed by -K
     if (!sc) {
         Sched1D e;
         e.K = -K;
-        std::vector<sb::Chunk1D> chunks;
-        auto mk = [&](int64_t start, int64_t S) {
-            sb::Chunk1D c;
-            c.start = start;
-            c.S = (int32_t)S;
-            c.pad = 0;
-            chunks.push_back(c);
-        };
-        e.comp_lo = P->phys_lo ? edge : 0;
-        e.comp_hi = n;
-        if (P->phys_hi) {
-            const int64_t start = std::max<int64_t>(e.comp_lo, (n - edge) / (2 * VEC) * (2 * VEC));
-            e.comp_hi = start;
-        }
-        if (P->phys_lo) mk(0, s_min);
-        if (P->phys_hi) mk(e.comp_hi, round_up((n - e.comp_hi + 31) / 32, SH::Q));
+        e.comp_lo = P->phys_lo ? HALF : 0;      // 16 B aligned: HALF % VEC == 0
+        e.comp_hi = P->phys_hi ? n - HALF : n;
         e.nchunks = 0;
-        e.nedge = (int)chunks.size();
-        if (!chunks.empty()) {
-            SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Chunk1D) * chunks.size()));
-            SB_CUDA(cudaMemcpy(e.d_chunks, chunks.data(), sizeof(sb::Chunk1D) * chunks.size(),
-                               cudaMemcpyHostToDevice));
-        }
+        e.nedge = (int)P->phys_lo + (int)P->phys_hi;
         auto ck = sb::compose1d_kernel<T, HALF>;
         const int smem = sb::compose1d_smem_bytes<T, HALF>();
         SB_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int occ = 0;
         SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ck, sb::C1_WARPS * 32, smem));
         e.blocks = P->num_sms * std::max(occ, 1);
-        auto ekern = sb::fused1d_edge_kernel<T, R, K, true, 3, false>;
-        SB_CUDA(cudaFuncSetAttribute(ekern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T)));
         auto cw = composed_weights(P->weights, K);
         e.cw.assign(cw.begin(), cw.end());
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }
-    // boundary chunks: exact level-by-level, side stream
-    if (sc->nedge > 0) {
-        sb::Fused1DParams<T, R> ep;
+    if (sc->nedge > 0) {   // boundary windows: exact level-by-level, side stream
+        sb::EdgeWindowParams<T, R> ep;
         ep.src = src + P->g.origin;
         ep.dst = dst + P->g.origin;
         ep.n = n;
-        ep.chunks = reinterpret_cast<const sb::Chunk1D*>(sc->d_chunks);
-        ep.nchunks = 0;
-        ep.total_warps = 0;
-        ep.counter = P->d_counter;
-        ep.trace = nullptr;
-        ep.phys_lo = P->phys_lo;
-        ep.phys_hi = P->phys_hi;
+        int b = 0;
+        if (P->phys_lo) ep.side[b++] = 0;
+        if (P->phys_hi) ep.side[b++] = 1;
         for (int i = 0; i < 2 * R + 1; i++) ep.w[i] = (T)P->weights[i];
         SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
         SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
-        sb::fused1d_edge_kernel<T, R, K, true, 3, false><<<(unsigned)sc->nedge, 32,
-            (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T), P->side_stream>>>(ep);
+        sb::edge_window_kernel<T, R, K, true><<<(unsigned)b, 32, 0, P->side_stream>>>(ep);
         SB_CUDA(cudaGetLastError());
         SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
         P->kernels_launched++;
@@ -245,13 +215,16 @@ int launch_fused1d_r(sb_plan* P, const T* src, T* dst, int k) {
     // composed path: FMA mode, depth >= 2, 16 B aligned halo, line long enough
     // (measured: it wins at k = 16 -- 3.6k vs 2.4k GStencil/s on C2 -- and loses at k <= 8,
     //  where the level-by-level kernel's memory pipeline is the better one)
-    if (FMA && compose && k >= (compose > 1 ? 2 : 16) && (R * k) % VEC == 0 &&
-        P->g.n[2] >= (int64_t)4 * 32 * 12 * 64 / (int)sizeof(T)) {
+    if (FMA && compose && compose1d_ok(P, k, compose > 1 ? 2 : 16)) {
         switch (k) {
             case 2: return launch_compose1d_k<T, R, 2>(P, src, dst);
             case 4: return launch_compose1d_k<T, R, 4>(P, src, dst);
             case 8: return launch_compose1d_k<T, R, 8>(P, src, dst);
             case 16: return launch_compose1d_k<T, R, 16>(P, src, dst);
+            case 32: return launch_compose1d_k<T, R, 32>(P, src, dst);
+            case 64:
+                if constexpr (R == 1) return launch_compose1d_k<T, R, 64>(P, src, dst);
+                break;
             default: break;
         }
     }

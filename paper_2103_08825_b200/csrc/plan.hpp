@@ -95,4 +95,15 @@ int launch_fused1d(sb_plan* P, int src_idx, int k);
 int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
 int make_tensor_maps(sb_plan* P, int geo, int box_h);
+
+// The composed 1D path (compose1d.cuh) serves depth k when the arithmetic is
+// FMA, R*k <= 64 taps each side, the halo is a whole number of 16 B vectors
+// and the line is long enough for the boundary windows.  `min_k` is 16 by
+// default (the level-by-level kernel wins below); depths 32 and 64 exist only
+// on this path.
+inline bool compose1d_ok(const sb_plan* P, int k, int min_k) {
+    const int vec = P->dtype == SB_F64 ? 2 : 4;
+    return P->d == 1 && P->arith == SB_ARITH_FMA && k >= min_k && P->r * k <= 64 &&
+           (P->r * k) % vec == 0 && P->dims[0] >= (int64_t)12288 * 8 / (int64_t)P->es;
+}
 }  // namespace sbh

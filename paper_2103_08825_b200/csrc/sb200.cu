@@ -108,9 +108,10 @@ int fused_kind(const sb_plan* P) {
 }
 
 // Supported fused depths (template instantiations) per kernel.
-bool fused_k_ok(int kind, int k) {
+bool fused_k_ok(const sb_plan* P, int kind, int k) {
     if (kind == KK_FUSED3D) return k >= 1 && k <= 4;
     if (kind == KK_FUSED2D) return k == 1 || k == 2 || k == 4 || k == 8;
+    if (k == 32 || k == 64) return compose1d_ok(P, k, 16);   // composed path only
     return k == 1 || k == 2 || k == 4 || k == 8 || k == 16;
 }
 
@@ -124,6 +125,10 @@ int largest_fused_k(int kind, int64_t steps, int kmax) {
 int default_k(int kind, const sb_plan* P) {
     if (kind == KK_FUSED3D) return P->shape == SB_BOX ? 2 : 4;
     if (kind == KK_FUSED2D) return 4;   // measured best on C3 (k=4: ~800, k=8: ~710 GStencil/s)
+    // 1D: the deepest composed depth in FMA mode (C2 k=32: ~3960 vs k=16: ~3670;
+    // C1 k=64: one launch for T=64), else the level-by-level kernel's 16
+    if (compose1d_ok(P, 64, 16)) return 64;
+    if (compose1d_ok(P, 32, 16)) return 32;
     return 16;
 }
 
@@ -184,7 +189,7 @@ int run_steps(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
     }
     if (slab) {
         // A slab plan runs one fused launch per exchange interval.
-        if (fused_k_ok(P->kind, (int)steps)) {
+        if (steps <= 64 && fused_k_ok(P, P->kind, (int)steps)) {
             *k_used = (int)steps;
             return launch_one<T, FMA>(P, (int)steps, 0, launches);
         }
@@ -300,10 +305,11 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     if (prob->kernel != SB_KERNEL_GENERIC && fk) {
         P->kind = fk;
         P->k = prob->k > 0 ? prob->k : default_k(fk, P);
-        if (!fused_k_ok(fk, P->k)) {
+        if (!fused_k_ok(P, fk, P->k)) {
             delete P;
             return fail(SB_ERR_ARG, "fused depth k=%d unsupported by the %s kernel", prob->k,
-                        fk == KK_FUSED3D ? "3D (1..4)" : fk == KK_FUSED2D ? "2D (1, 2, 4, 8)" : "1D (1, 2, 4, 8, 16)");
+                        fk == KK_FUSED3D ? "3D (1..4)" : fk == KK_FUSED2D ? "2D (1, 2, 4, 8)"
+                        : "1D (1, 2, 4, 8, 16; 32, 64 in FMA mode with r*k <= 64)");
         }
     } else {
         P->kind = KK_GENERIC;

@@ -26,8 +26,9 @@ import numpy as np
 
 from .core import GridError, validate
 
-# fused depths the slab plans accept per launch (see sb200.cu fused_k_ok)
-_FUSED_KS = {1: (1, 2, 4, 8, 16), 2: (1, 2, 4, 8), 3: (1, 2, 3, 4)}
+# fused depths the slab plans accept per launch (see sb200.cu fused_k_ok;
+# 1D depths 32 and 64 exist only on the composed path: FMA mode, r*k <= 64)
+_FUSED_KS = {1: (1, 2, 4, 8, 16, 32, 64), 2: (1, 2, 4, 8), 3: (1, 2, 3, 4)}
 
 
 def split_extent(n: int, world: int) -> list[tuple[int, int]]:

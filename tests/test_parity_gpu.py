@@ -161,6 +161,68 @@ def test_linearity_full_c2():
     assert np_oracle.max_rel_error(sab, 0.5 * sa + 0.25 * sb) <= 1e-12
 
 
+# --- composed 1D path (FMA, depth k as one (2rk+1)-tap stencil + exact boundary windows)
+
+@pytest.mark.parametrize("cfg,k", [("c1", 16), ("c1", 32), ("c1", 64), ("c2", 16), ("c2", 32)])
+@pytest.mark.parametrize("n", [12288, 12289, 100003])
+@pytest.mark.parametrize("halo", ["full", "zero"])
+def test_composed1d_within_fp64_bar(cfg, k, n, halo):
+    spec = config_spec(cfg)
+    box = seeded_box((n,), spec.r, seed=n + k, halo=halo)
+    T = 2 * k + 7                            # full-depth launches plus a shallower tail
+    with Plan(spec, (n,), k=k, arith="fma") as p:
+        p.upload(box)
+        t = p.run(T)
+        got = p.download()
+    assert t.kernel_name in ("compose1d_kernel", "fused1d_kernel")
+    want = oracle(spec, box, T)
+    assert np_oracle.max_rel_error(interior(got, spec.r), interior(want, spec.r)) <= FP64_TOL
+    assert np.array_equal(got[:spec.r], box[:spec.r]) and np.array_equal(got[-spec.r:], box[-spec.r:])
+
+
+def test_composed1d_boundary_values_exact_level_by_level():
+    # outputs within r*k of the Dirichlet halo come from the exact window kernel:
+    # with an impulse next to the boundary they match the level-by-level oracle
+    spec = config_spec("c1")
+    n = 20000
+    box = np.zeros(n + 2)
+    box[1:40] = np.linspace(1.0, 2.0, 39)
+    box[0] = 3.0
+    box[-1] = -1.0
+    box[-40:-1] = 0.5
+    got = sweep(spec, box, 64, arith="fma", k=64)
+    want = oracle(spec, box, 64)
+    assert np_oracle.max_rel_error(got, want) <= FP64_TOL
+
+
+def test_composed1d_fp32_k32():
+    spec = config_spec("c2")
+    box32 = seeded_box((100003,), 2, seed=4).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 2, offs, [float(np.float32(w)) for w in ws], 64)
+    got = sweep(spec, box32, 64, arith="fma", k=32)
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+def test_c1_full_size_one_launch_k64():
+    spec = config_spec("c1")
+    box = seeded_box((1 << 20,), 1)
+    with Plan(spec, (1 << 20,), k=64, arith="fma") as p:
+        p.upload(box)
+        t = p.run(64)
+        got = p.download()
+    assert t.launches == 2 and t.kernel_name == "compose1d_kernel"   # composed + boundary windows
+    assert np_oracle.max_rel_error(got, oracle(spec, box, 64)) <= FP64_TOL
+
+
+def test_composed_depth_rejected_when_unavailable():
+    spec = config_spec("c2")
+    with pytest.raises(ValueError):
+        Plan(spec, (100000,), k=64, arith="fma")       # r*k = 128 > 64
+    with pytest.raises(ValueError):
+        Plan(spec, (100000,), k=32, arith="exact")     # composed path is FMA-only
+
+
 def test_plan_reuse_and_timing():
     spec = config_spec("c2")
     box = seeded_box((100000,), 2)

@@ -121,3 +121,22 @@ def test_single_gpu_slab_emulation_bit_identical(cfg, dims, k, g):
     offs, ws = canonical(spec)
     want = c_oracle.sweep(gbox, spec.r, offs, ws, steps)
     assert got.tobytes() == want[spec.r:spec.r + dims[0]].tobytes()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,k,g", [("c2", 32, 2), ("c1", 64, 3), ("c2", 16, 3)])
+def test_single_gpu_slab_emulation_composed_matches_whole_line(cfg, k, g):
+    # composed path (FMA): slabs reproduce a whole-line plan bit for bit --
+    # every output takes the same composed taps or the same boundary window
+    spec = config_spec(cfg)
+    dims = (300001,)
+    gbox = seeded_box(dims, spec.r, seed=5)
+    sweeps = [SlabSweep(spec, dims, rank=r, world=g, k=k, arith="fma", device=0) for r in range(g)]
+    for s in sweeps:
+        s.upload(s.local_box(gbox))
+    steps = 3 * k + 1
+    run_local(sweeps, steps)
+    got = np.concatenate([s.download()[s.geom.interior_slice()] for s in sweeps], axis=0)
+    from paper_2103_08825_b200.plan import sweep
+    whole = sweep(spec, gbox, steps, arith="fma", k=k)
+    assert got.tobytes() == whole[spec.r:spec.r + dims[0]].tobytes()
