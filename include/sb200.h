@@ -15,6 +15,9 @@
  *                       (kernels.py:120-134) and the k-level time jam
  *                       jam_sweep (timejam.py:288-304)
  *   sb_download      <- GridBuffer.natural_interior (core.py:308-316)
+ *   sb_upload_async / sb_download_async / sb_synchronize
+ *                    <- (no reference counterpart: stream-ordered transfers
+ *                       for overlapping independent grids' sweeps)
  *   sb_plan_destroy  <- (buffers going out of scope)
  *   sb_last_error    <- exception messages of SpecError/GridError
  *                       (core.py:38-43)
@@ -105,6 +108,16 @@ int sb_host_elems(const sb_plan *plan, int64_t *elems);
 int sb_upload(sb_plan *plan, const void *host, size_t bytes);
 /* Device (current buffer) -> host box, halo included. */
 int sb_download(sb_plan *plan, void *host, size_t bytes);
+
+/* Stream-ordered forms of sb_upload / sb_download on the plan stream: they
+ * return once the copy is enqueued.  `host` must stay valid (and should be
+ * page-locked, e.g. cudaHostAlloc, for the copy to overlap other work) until
+ * sb_synchronize -- used to overlap one grid's transfers with another
+ * plan's sweep (pipelined end-to-end sweeps of independent grids). */
+int sb_upload_async(sb_plan *plan, const void *host, size_t bytes);
+int sb_download_async(sb_plan *plan, void *host, size_t bytes);
+/* Wait for everything enqueued on the plan stream; reports kernel errors. */
+int sb_synchronize(sb_plan *plan);
 
 /* Advance `steps` time steps, synchronously; fills *timing if non-NULL.
  * Slab plans (ghost_lo/hi > 0) accept steps <= min ghost depth / r. */

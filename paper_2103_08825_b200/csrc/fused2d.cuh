@@ -24,6 +24,7 @@
 // replaced by the Dirichlet halo (global read), beyond the halo shell by 0;
 // slab (ghost) sides along y compute normally.
 #pragma once
+#include <climits>
 #include "common.cuh"
 #include "fused1d.cuh"   // cp.async helpers, Vec16
 
@@ -57,14 +58,19 @@ struct Fused2DParams {
     T w[9];                  // w[(dy+1)*3 + (dx+1)]; star uses 5 entries
 };
 
-// Strip geometry: the computed strip origin xc = x0 - (K-1) must be 16 B
-// aligned (staged chunks), so the output width is a multiple of the 16 B
-// vector and strip 0 starts at X0 <= 0 with X0 == K-1 (mod VEC).
+// Strip geometry, lane aligned: the K-1 recomputed columns on each side of a
+// strip are rounded up to whole lanes (HL columns), so lanes either own four
+// output columns or none -- every storing lane writes whole 16 B vectors and
+// no lane takes a partial-store path except on the grid's last strip.  The
+// computed strip origin xc = x0 - HL is then 16 B aligned for any x0 that is
+// a multiple of VX (output strips start at multiples of TXO).
 template <typename T, int K>
 struct F2Tile {
     static constexpr int VEC = 16 / (int)sizeof(T);
-    static constexpr int TXO = ((F2_CW - 2 * (K - 1)) / VEC) * VEC;
-    static constexpr int X0 = ((K - 1) % VEC == 0) ? 0 : ((K - 1) % VEC) - VEC;
+    static constexpr int HL = F2_VX * ((K - 1 + F2_VX - 1) / F2_VX);
+    static constexpr int TXO = F2_CW - 2 * HL;
+    static constexpr int X0 = 0;
+    static_assert(HL % VEC == 0 && TXO > 0, "strip geometry");
 };
 
 template <typename T>   // one element (4 or 8 B), zero-filled when !valid
@@ -134,7 +140,7 @@ fused2d_kernel(const Fused2DParams<T> P) {
         const unsigned next_raw = claim_issue();        // resolved after this item
         const Item2D it = P.sched[item];
         const int x0 = TL::X0 + it.tix * TL::TXO;       // output strip origin
-        const int xc = x0 - (K - 1);                    // computed strip origin (16 B aligned)
+        const int xc = x0 - TL::HL;                     // computed strip origin (16 B aligned)
         const int ys0 = it.ys0, ys1 = it.ys1;
         const int p_first = ys0 - K;
         const int M = (ys1 - ys0) + 2 * K;
@@ -151,6 +157,9 @@ fused2d_kernel(const Fused2DParams<T> P) {
             store_mask |= (unsigned)(cj >= 0 && cj < TL::TXO && x >= 0 && x < P.nx) << j;
         }
         const bool warp_out = __any_sync(0xffffffffu, out_mask != 0);   // strip touches the x halo
+        // rows outside [ylo, yhi) on a physical side are Dirichlet halo
+        const int ylo = P.phys_lo ? 0 : INT_MIN / 2, yhi = P.phys_hi ? P.ny : INT_MAX / 2;
+        T* const out_base = P.dst + P.origin + (int64_t)(p_first - K) * P.sy + col[0];   // row of t = 0
         const int ecol = lane == 0 ? xc - 1 : xc + F2_CW;   // strip-edge halo column (lanes 0, 31)
         const bool eload = (lane == 0 || lane == 31) && ecol >= -1 && ecol <= P.nx;
 
@@ -191,20 +200,24 @@ fused2d_kernel(const Fused2DParams<T> P) {
             __syncwarp();                                   // slot t-1 fully read before restaging
             stage(t + F2_DEPTH - 1);
             const int a0 = p_first + t;
+            // no level of this row touches a physical y halo and the strip no x halo
+            const bool plain = !warp_out && a0 - K >= ylo && a0 - 1 < yhi;
 #pragma unroll
             for (int l = 1; l <= K; l++) {
                 T u[F2_VX + 2];
                 const T left = __shfl_up_sync(0xffffffffu, v[F2_VX - 1], 1);
                 const T right = __shfl_down_sync(0xffffffffu, v[0], 1);
-                u[0] = lane == 0 ? edge : left;
-                u[F2_VX + 1] = lane == 31 ? edge : right;
+                // the strip-edge halo column matters only at level 1; above it the
+                // strip's outermost columns are garbage anyway (overlapped strips)
+                u[0] = (l == 1 && lane == 0) ? edge : left;
+                u[F2_VX + 1] = (l == 1 && lane == 31) ? edge : right;
 #pragma unroll
                 for (int j = 0; j < F2_VX; j++) u[j + 1] = v[j];
                 T done[F2_VX];
                 f2_push<T, BOX, FMA>(u, Pm[l - 1], P0[l - 1], done, P.w);
                 const int yc = a0 - l;                      // completed level-l row
-                const bool y_out = (P.phys_lo && yc < 0) || (P.phys_hi && yc >= P.ny);
-                if (y_out || warp_out) {                    // (warp-uniform) Dirichlet halo, same at every level
+                const bool y_out = yc < ylo || yc >= yhi;
+                if (!plain && (y_out || warp_out)) {        // (warp-uniform) Dirichlet halo, same at every level
                     const bool y_shell = yc >= -1 && yc <= P.ny;
                     const bool y_alloc = yc >= P.row_lo && yc < P.row_hi;
                     const T* rowp = P.src + P.origin + (int64_t)yc * P.sy;
@@ -221,21 +234,20 @@ fused2d_kernel(const Fused2DParams<T> P) {
                 if (l < K) {
 #pragma unroll
                     for (int j = 0; j < F2_VX; j++) v[j] = done[j];
-                    edge = T(0);                            // beyond level 0 the strip edge is garbage
                 } else if (yc >= ys0 && yc < ys1) {
-                    T* rowp = P.dst + P.origin + (int64_t)yc * P.sy;
+                    T* rowp = out_base + (int64_t)t * P.sy;    // row yc, column col[0]
                     if (store_mask == (1u << F2_VX) - 1) {  // whole 16 B-aligned chunk: vector stores
 #pragma unroll
                         for (int c = 0; c < F2_VX / VEC; c++) {
                             V pack;
 #pragma unroll
                             for (int e = 0; e < VEC; e++) reinterpret_cast<T*>(&pack)[e] = done[c * VEC + e];
-                            *reinterpret_cast<V*>(rowp + col[0] + c * VEC) = pack;
+                            *reinterpret_cast<V*>(rowp + c * VEC) = pack;
                         }
-                    } else {
+                    } else if (store_mask) {                // last strip only: columns past nx
 #pragma unroll
                         for (int j = 0; j < F2_VX; j++)
-                            if ((store_mask >> j) & 1) rowp[col[j]] = done[j];
+                            if ((store_mask >> j) & 1) rowp[j] = done[j];
                     }
                 }
             }

@@ -237,6 +237,50 @@ int max_slab_steps(const sb_plan* P) {
 }  // namespace
 
 // ===================================================================== C ABI
+namespace sbh {
+
+// Host box -> buf[0], then the halo/ghost into buf[1] too (kernels never
+// write it).  1D copies only the two ends (pad + halo); 2D/3D copy the whole
+// buffer (cheap next to those sweeps).  Stream-ordered, no host sync.
+int enqueue_upload(sb_plan* P, const void* host, size_t bytes) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    if (bytes != (size_t)P->host_elems * P->es)
+        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
+                    (long long)(P->host_elems * (int64_t)P->es));
+    SB_CUDA(cudaSetDevice(P->device));
+    char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
+    SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, host, P->host_row_elems * P->es,
+                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyHostToDevice, P->stream));
+    if (P->d == 1) {
+        const size_t lo = (size_t)P->g.origin, hi = (size_t)(P->g.origin + P->g.n[2]);
+        char* b0 = reinterpret_cast<char*>(P->buf[0]);
+        char* b1 = reinterpret_cast<char*>(P->buf[1]);
+        SB_CUDA(cudaMemcpyAsync(b1, b0, lo * P->es, cudaMemcpyDeviceToDevice, P->stream));
+        SB_CUDA(cudaMemcpyAsync(b1 + hi * P->es, b0 + hi * P->es, (P->buf_elems - hi) * P->es,
+                                cudaMemcpyDeviceToDevice, P->stream));
+    } else {
+        SB_CUDA(cudaMemcpyAsync(P->buf[1], P->buf[0], P->buf_elems * P->es, cudaMemcpyDeviceToDevice, P->stream));
+    }
+    P->cur = 0;
+    P->uploaded = true;
+    return SB_OK;
+}
+
+int enqueue_download(sb_plan* P, void* host, size_t bytes) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "download before upload");
+    if (bytes != (size_t)P->host_elems * P->es)
+        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
+                    (long long)(P->host_elems * (int64_t)P->es));
+    SB_CUDA(cudaSetDevice(P->device));
+    const char* src = reinterpret_cast<const char*>(P->buf[P->cur]) + P->host_dst_offset * P->es;
+    SB_CUDA(cudaMemcpy2DAsync(host, P->host_row_elems * P->es, src, P->px * P->es,
+                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyDeviceToHost, P->stream));
+    return SB_OK;
+}
+
+}  // namespace sbh
+
 extern "C" {
 
 const char* sb_last_error(void) { return g_err.c_str(); }
@@ -440,32 +484,28 @@ int sb_host_elems(const sb_plan* P, int64_t* elems) {
 }
 
 int sb_upload(sb_plan* P, const void* host, size_t bytes) {
-    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
-    if (bytes != (size_t)P->host_elems * P->es)
-        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
-                    (long long)(P->host_elems * (int64_t)P->es));
-    SB_CUDA(cudaSetDevice(P->device));
-    char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
-    SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, host, P->host_row_elems * P->es,
-                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyHostToDevice, P->stream));
-    SB_CUDA(cudaMemcpyAsync(P->buf[1], P->buf[0], P->buf_elems * P->es, cudaMemcpyDeviceToDevice, P->stream));
+    const int rc = sbh::enqueue_upload(P, host, bytes);
+    if (rc != SB_OK) return rc;
     SB_CUDA(cudaStreamSynchronize(P->stream));
-    P->cur = 0;
-    P->uploaded = true;
     return SB_OK;
 }
 
 int sb_download(sb_plan* P, void* host, size_t bytes) {
-    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
-    if (!P->uploaded) return fail(SB_ERR_STATE, "download before upload");
-    if (bytes != (size_t)P->host_elems * P->es)
-        return fail(SB_ERR_GRID, "host box has %zu bytes, expected %lld", bytes,
-                    (long long)(P->host_elems * (int64_t)P->es));
-    SB_CUDA(cudaSetDevice(P->device));
-    const char* src = reinterpret_cast<const char*>(P->buf[P->cur]) + P->host_dst_offset * P->es;
-    SB_CUDA(cudaMemcpy2DAsync(host, P->host_row_elems * P->es, src, P->px * P->es,
-                              P->host_row_elems * P->es, P->host_rows, cudaMemcpyDeviceToHost, P->stream));
+    const int rc = sbh::enqueue_download(P, host, bytes);
+    if (rc != SB_OK) return rc;
     SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
+}
+
+int sb_upload_async(sb_plan* P, const void* host, size_t bytes) { return sbh::enqueue_upload(P, host, bytes); }
+
+int sb_download_async(sb_plan* P, void* host, size_t bytes) { return sbh::enqueue_download(P, host, bytes); }
+
+int sb_synchronize(sb_plan* P) {
+    if (!P) return fail(SB_ERR_ARG, "NULL plan");
+    SB_CUDA(cudaSetDevice(P->device));
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    SB_CUDA(cudaGetLastError());
     return SB_OK;
 }
 

@@ -134,6 +134,21 @@ class Plan:
         _abi.check(self._lib.sb_download(self._h, out.ctypes.data, out.nbytes))
         return out
 
+    def upload_async(self, box: np.ndarray) -> None:
+        """Stream-ordered upload: returns once enqueued; `box` (ideally pinned
+        memory) must stay alive and unmodified until :meth:`synchronize`."""
+        self._check_box(box)
+        _abi.check(self._lib.sb_upload_async(self._h, box.ctypes.data, box.nbytes))
+
+    def download_async(self, out: np.ndarray) -> np.ndarray:
+        """Stream-ordered download into `out`; valid after :meth:`synchronize`."""
+        self._check_box(out)
+        _abi.check(self._lib.sb_download_async(self._h, out.ctypes.data, out.nbytes))
+        return out
+
+    def synchronize(self) -> None:
+        _abi.check(self._lib.sb_synchronize(self._h))
+
     # -- compute
     def run(self, steps: int) -> Timing:
         t = _abi.SbTiming()

@@ -332,3 +332,32 @@ def test_c3_full_size_fma(cfg):
     got = sweep(spec, box, 16, arith="fma", k=8)
     want = oracle(spec, box, 16)
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
+
+
+def test_async_transfers_pipelined_two_plans():
+    # sb_upload_async / sb_launch / sb_download_async on two plans and two
+    # streams (the bench's pipelined e2e): same bytes as the synchronous calls
+    import torch
+    spec = config_spec("c2")
+    n = 200003
+    boxes = [seeded_box((n,), 2, seed=s) for s in (1, 2, 3, 4)]
+    want = [sweep(spec, b, 40, arith="fma") for b in boxes]
+    plans = [Plan(spec, (n,), arith="fma") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    ins = [torch.from_numpy(b).pin_memory() for b in boxes]
+    outs = [torch.empty_like(i).pin_memory() for i in ins]
+    try:
+        for p, s in zip(plans, streams):
+            p.set_stream(s.cuda_stream)
+        for i in range(4):
+            p = plans[i % 2]
+            p.upload_async(ins[i].numpy())
+            p.launch(40)
+            p.download_async(outs[i].numpy())
+        for p in plans:
+            p.synchronize()
+        for o, w in zip(outs, want):
+            assert o.numpy().tobytes() == w.tobytes()
+    finally:
+        for p in plans:
+            p.close()
