@@ -420,7 +420,7 @@ def run_gpu_arm(args):
                 p.launch(T)
                 p.download_async(outs[i % NP].numpy())
 
-            for i in range(NP):                                  # warm-up: every plan once
+            for i in range(2 * NP):                              # warm-up: eager + graph capture per plan
                 pipelined(i)
             for p in plans:
                 p.synchronize()

@@ -49,6 +49,19 @@ struct Chunk1DHost {
 
 }  // namespace sbh
 
+// A captured sweep: the launch sequence of `steps` steps starting from
+// buffer `cur0`, replayed with one cudaGraphLaunch (sb200.cu run_graphed).
+struct SweepGraph {
+    int64_t steps = 0;
+    int cur0 = 0, cur1 = 0;
+    int hits = 0;
+    cudaGraphExec_t exec = nullptr;
+    bool failed = false;
+    int64_t kernels = 0, launches = 0;
+    int k_used = 1;
+    const char* last_kernel = nullptr;
+};
+
 struct sb_plan {
     int d = 0, r = 0, shape = 0, nw = 0, dtype = 0, arith = 0, kreq = 0, kernel_req = 0;
     int device = 0;
@@ -73,6 +86,7 @@ struct sb_plan {
     void* d_w = nullptr;
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<sbh::Sched1D> sched1d;
+    std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
     CUtensorMap tmap[2][2];                // TMA descriptors [geometry][buffer] (3D)
     bool tmap_ok[2] = {false, false};
     unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)

@@ -219,6 +219,59 @@ int dispatch_run(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
                : run_steps<float, false>(P, steps, launches, k_used);
 }
 
+// CUDA-graph replay of repeated sweeps.  The first sweep of a given
+// (steps, starting buffer) runs eagerly (it also performs every first-use
+// setup: schedules, smem attributes, tensor maps); the second is captured
+// from the plan stream (side-stream fork/join included) and instantiated;
+// later ones replay it with a single cudaGraphLaunch -- the host cost of a
+// short sweep (C1: one composed launch + its boundary windows + 4 event
+// calls) drops to one call.  SB200_GRAPHS=0 disables it.
+int run_graphed(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
+    static const bool enabled = env_double("SB200_GRAPHS", 1) != 0 && !getenv("SB200_TRACE");
+    if (!enabled || steps == 0) return dispatch_run(P, steps, launches, k_used);
+    SweepGraph* g = nullptr;
+    for (auto& e : P->graphs)
+        if (e.steps == steps && e.cur0 == P->cur) g = &e;
+    if (!g) {
+        if (P->graphs.size() >= 16) return dispatch_run(P, steps, launches, k_used);
+        SweepGraph e;
+        e.steps = steps;
+        e.cur0 = P->cur;
+        P->graphs.push_back(e);
+        g = &P->graphs.back();
+    }
+    if (g->failed || ++g->hits < 2) return dispatch_run(P, steps, launches, k_used);
+    if (!g->exec) {
+        const int cur_before = P->cur;
+        const int64_t kernels_before = P->kernels_launched;
+        cudaGraph_t graph = nullptr;
+        SB_CUDA(cudaStreamBeginCapture(P->stream, cudaStreamCaptureModeThreadLocal));
+        const int rc = dispatch_run(P, steps, &g->launches, &g->k_used);
+        const cudaError_t ec = cudaStreamEndCapture(P->stream, &graph);
+        g->cur1 = P->cur;
+        g->kernels = P->kernels_launched - kernels_before;
+        g->last_kernel = P->last_kernel;
+        P->cur = cur_before;                       // nothing has executed yet
+        P->kernels_launched = kernels_before;
+        if (rc != SB_OK || ec != cudaSuccess ||
+            cudaGraphInstantiate(&g->exec, graph, 0) != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();                    // clear; fall back to eager launches
+            g->failed = true;
+            g->exec = nullptr;
+            return dispatch_run(P, steps, launches, k_used);
+        }
+        cudaGraphDestroy(graph);
+    }
+    SB_CUDA(cudaGraphLaunch(g->exec, P->stream));
+    P->cur = g->cur1;
+    P->kernels_launched += g->kernels;
+    P->last_kernel = g->last_kernel;
+    *launches = g->launches;
+    *k_used = g->k_used;
+    return SB_OK;
+}
+
 const char* kernel_name(const sb_plan* P) {
     if (P->last_kernel) return P->last_kernel;
     if (P->kind == KK_FUSED1D) return "fused1d_kernel";
@@ -306,6 +359,8 @@ void sb_plan_destroy(sb_plan* P) {
     if (P->d_trace) cudaFree(P->d_trace);
     for (auto& e : P->sched1d)
         if (e.d_chunks) cudaFree(e.d_chunks);
+    for (auto& g : P->graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
     for (int i = 0; i < 2; i++)
         if (P->ev[i]) cudaEventDestroy(P->ev[i]);
     if (P->fork_ev) cudaEventDestroy(P->fork_ev);
@@ -518,7 +573,7 @@ int sb_launch(sb_plan* P, int64_t steps) {
     SB_CUDA(cudaSetDevice(P->device));
     int64_t launches = 0;
     int k_used = 1;
-    return dispatch_run(P, steps, &launches, &k_used);
+    return run_graphed(P, steps, &launches, &k_used);
 }
 
 int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
@@ -532,7 +587,7 @@ int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {
     int k_used = 1;
     const int64_t kernels_before = P->kernels_launched;
     SB_CUDA(cudaEventRecord(P->ev[0], P->stream));
-    int rc = dispatch_run(P, steps, &launches, &k_used);
+    int rc = run_graphed(P, steps, &launches, &k_used);
     if (rc != SB_OK) return rc;
     SB_CUDA(cudaEventRecord(P->ev[1], P->stream));
     SB_CUDA(cudaEventSynchronize(P->ev[1]));
