@@ -15,6 +15,8 @@
  *                       (kernels.py:120-134) and the k-level time jam
  *                       jam_sweep (timejam.py:288-304)
  *   sb_download      <- GridBuffer.natural_interior (core.py:308-316)
+ *   sb_step_box      <- scalar_step(..., ranges=...) as driven by the tiled
+ *                       runner (tiling.py:353-354)
  *   sb_upload_async / sb_download_async / sb_synchronize
  *                    <- (no reference counterpart: stream-ordered transfers
  *                       for overlapping independent grids' sweeps)
@@ -125,6 +127,13 @@ int sb_run(sb_plan *plan, int64_t steps, sb_timing *timing);
 
 /* Same, asynchronously on the plan stream (no host sync, no timing). */
 int sb_launch(sb_plan *plan, int64_t steps);
+
+/* One step restricted to the interior sub-box lo[a] <= i_a < hi[a] (first d
+ * entries, slowest axis first): the reference's `ranges` argument
+ * (scalar_step, kernels.py:120-134 / _region, kernels.py:88-100).  Writes
+ * only the box of the other buffer (the rest of it is stale), then swaps
+ * buffers; synchronous.  Whole-grid plans only. */
+int sb_step_box(sb_plan *plan, const int64_t *lo, const int64_t *hi);
 
 /* Run on an external stream (e.g. torch's current stream); NULL restores
  * the plan's own stream. */

@@ -22,7 +22,7 @@ SB_KERNEL_AUTO, SB_KERNEL_GENERIC, SB_KERNEL_FUSED = 0, 1, 2
 EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_download", "sb_run", "sb_launch", "sb_set_stream", "sb_device_view",
            "sb_plan_k", "sb_kernel_count", "sb_last_error", "sb_abi_version", "sb_device_count",
-           "sb_upload_async", "sb_download_async", "sb_synchronize")
+           "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box")
 
 
 class SbProblem(ctypes.Structure):
@@ -69,6 +69,7 @@ def load():
     lib.sb_upload_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_download_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_synchronize.argtypes = [P]
+    lib.sb_step_box.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     lib.sb_run.argtypes = [P, ctypes.c_int64, ctypes.POINTER(SbTiming)]
     lib.sb_launch.argtypes = [P, ctypes.c_int64]
     lib.sb_set_stream.argtypes = [P, ctypes.c_void_p]
@@ -82,7 +83,7 @@ def load():
     lib.sb_device_count.restype = ctypes.c_int
     for name in ("sb_plan_create", "sb_host_elems", "sb_upload", "sb_download", "sb_run",
                  "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k", "sb_kernel_count",
-                 "sb_upload_async", "sb_download_async", "sb_synchronize"):
+                 "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -14,12 +14,18 @@ namespace sb {
 constexpr int kGenericThreads = 256;
 constexpr int kGenericMaxW = 1024;
 
-// Computes axis-`slab_axis` positions [lo, hi) (may include ghost planes of
-// a slab side) and the full interior of the other axes.
+// Interior sub-box computed by one launch: positions base[a] .. base[a] +
+// ext[a] - 1 on each canonical axis (z, y, x).  The full sweep uses the whole
+// interior (on a slab axis extended into the ghost planes); sb_step_box
+// passes the reference's `ranges` (kernels.py:88-108).
+struct Box3 {
+    int64_t base[3];
+    int64_t ext[3];
+};
+
 template <typename T, bool FMA>
 __global__ void __launch_bounds__(kGenericThreads)
-generic_step_kernel(const T* __restrict__ src, T* __restrict__ dst, Geom g,
-                    int64_t lo, int64_t hi, int nw,
+generic_step_kernel(const T* __restrict__ src, T* __restrict__ dst, Geom g, Box3 b, int nw,
                     const int64_t* __restrict__ lin, const T* __restrict__ w) {
     __shared__ int64_t s_lin[kGenericMaxW];
     __shared__ T s_w[kGenericMaxW];
@@ -29,17 +35,12 @@ generic_step_kernel(const T* __restrict__ src, T* __restrict__ dst, Geom g,
     }
     __syncthreads();
 
-    int64_t ext[3] = {g.n[0], g.n[1], g.n[2]};
-    int64_t base[3] = {0, 0, 0};
-    ext[g.slab_axis] = hi - lo;
-    base[g.slab_axis] = lo;
-
-    const int64_t rows = ext[0] * ext[1];
-    const int64_t x = base[2] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (x >= base[2] + ext[2]) return;
+    const int64_t rows = b.ext[0] * b.ext[1];
+    const int64_t x = b.base[2] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (x >= b.base[2] + b.ext[2]) return;
     for (int64_t row = blockIdx.y; row < rows; row += gridDim.y) {
-        const int64_t z = base[0] + row / ext[1];
-        const int64_t y = base[1] + row % ext[1];
+        const int64_t z = b.base[0] + row / b.ext[1];
+        const int64_t y = b.base[1] + row % b.ext[1];
         const int64_t p = g.origin + z * g.sz + y * g.sy + x;
         T acc = acc_first<T, FMA>(s_w[0], src[p + s_lin[0]]);
         for (int i = 1; i < nw; i++) acc = acc_term<T, FMA>(acc, s_w[i], src[p + s_lin[i]]);

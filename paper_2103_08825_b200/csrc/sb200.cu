@@ -135,18 +135,28 @@ int default_k(int kind, const sb_plan* P) {
 // ---------------------------------------------------------------- launches
 
 template <typename T, bool FMA>
-int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
-    sb::Geom g = P->g;
-    int64_t ext[3] = {g.n[0], g.n[1], g.n[2]};
-    ext[g.slab_axis] = hi - lo;
-    if (ext[0] <= 0 || ext[1] <= 0 || ext[2] <= 0) return SB_OK;
-    const int64_t rows = ext[0] * ext[1];
-    dim3 grid((unsigned)((ext[2] + sb::kGenericThreads - 1) / sb::kGenericThreads),
+int launch_generic_box(sb_plan* P, const T* src, T* dst, const sb::Box3& b) {
+    if (b.ext[0] <= 0 || b.ext[1] <= 0 || b.ext[2] <= 0) return SB_OK;
+    const int64_t rows = b.ext[0] * b.ext[1];
+    dim3 grid((unsigned)((b.ext[2] + sb::kGenericThreads - 1) / sb::kGenericThreads),
               (unsigned)std::min<int64_t>(rows, 65535));
     sb::generic_step_kernel<T, FMA><<<grid, sb::kGenericThreads, 0, P->stream>>>(
-        src, dst, g, lo, hi, P->nw, P->d_lin, reinterpret_cast<const T*>(P->d_w));
+        src, dst, P->g, b, P->nw, P->d_lin, reinterpret_cast<const T*>(P->d_w));
     SB_CUDA(cudaGetLastError());
     return SB_OK;
+}
+
+// Whole interior; on the slab axis positions [lo, hi) (ghost planes included).
+template <typename T, bool FMA>
+int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
+    sb::Box3 b;
+    for (int a = 0; a < 3; a++) {
+        b.base[a] = 0;
+        b.ext[a] = P->g.n[a];
+    }
+    b.base[P->g.slab_axis] = lo;
+    b.ext[P->g.slab_axis] = hi - lo;
+    return launch_generic_box<T, FMA>(P, src, dst, b);
 }
 
 // One launch advancing k levels from buf[cur] into buf[cur^1].
@@ -574,6 +584,45 @@ int sb_launch(sb_plan* P, int64_t steps) {
     int64_t launches = 0;
     int k_used = 1;
     return run_graphed(P, steps, &launches, &k_used);
+}
+
+int sb_step_box(sb_plan* P, const int64_t* lo, const int64_t* hi) {
+    if (!P || !lo || !hi) return fail(SB_ERR_ARG, "NULL argument");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "run before upload");
+    if (!(P->phys_lo && P->phys_hi)) return fail(SB_ERR_GRID, "sb_step_box needs a whole-grid plan (no ghost sides)");
+    sb::Box3 b;
+    for (int a = 0; a < 3; a++) {
+        b.base[a] = 0;
+        b.ext[a] = 1;
+    }
+    for (int a = 0; a < P->d; a++) {
+        const int ca = 3 - P->d + a;   // canonical axis
+        if (lo[a] < 0 || hi[a] > P->dims[a])
+            return fail(SB_ERR_GRID, "range (%lld, %lld) outside axis %d of extent %lld", (long long)lo[a],
+                        (long long)hi[a], a, (long long)P->dims[a]);
+        b.base[ca] = lo[a];
+        b.ext[ca] = std::max<int64_t>(0, hi[a] - lo[a]);
+    }
+    SB_CUDA(cudaSetDevice(P->device));
+    const bool fma = P->arith == SB_ARITH_FMA;
+    int rc;
+    if (P->dtype == SB_F64) {
+        auto src = reinterpret_cast<const double*>(P->buf[P->cur]);
+        auto dst = reinterpret_cast<double*>(P->buf[P->cur ^ 1]);
+        rc = fma ? launch_generic_box<double, true>(P, src, dst, b)
+                 : launch_generic_box<double, false>(P, src, dst, b);
+    } else {
+        auto src = reinterpret_cast<const float*>(P->buf[P->cur]);
+        auto dst = reinterpret_cast<float*>(P->buf[P->cur ^ 1]);
+        rc = fma ? launch_generic_box<float, true>(P, src, dst, b)
+                 : launch_generic_box<float, false>(P, src, dst, b);
+    }
+    if (rc != SB_OK) return rc;
+    P->cur ^= 1;
+    P->kernels_launched++;
+    P->last_kernel = "generic_step_kernel";
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
 }
 
 int sb_run(sb_plan* P, int64_t steps, sb_timing* t) {

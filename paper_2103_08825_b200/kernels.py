@@ -41,20 +41,42 @@ def _points(grid) -> int:
 
 
 def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> None:
-    """One sweep ``dst = S(src)`` on the GPU (signature of kernels.py:120-134)."""
+    """One sweep ``dst = S(src)`` on the GPU (signature of kernels.py:120-134).
+
+    ``ranges`` = [(lo, hi)] per axis restricts the step to that interior
+    sub-box, as the reference's tiled runner drives it (tiling.py:353-354):
+    the device computes only the box (sb_step_box) and only the box of
+    ``dst`` is written; counters count the box's points (kernels.py:127-134).
+    """
     _check_pair(src, dst)
     validate(spec)
-    if ranges is not None:
-        raise GridError("b200 step does not take ranges; the tile runner is not "
-                        "driven through sb200 (GPU tiles are internal to the kernels)")
+    r = spec.r
     box = np.ascontiguousarray(compact_view(src), dtype=np.float64)
-    with Plan(spec, tuple(src.dims), arith=arith, k=1) as p:
-        p.upload(box)
-        p.run(1)
-        out = p.download()
-    interior_view(dst)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
-    if counters is not None:
+    if ranges is not None:
+        ranges = [(int(lo), int(hi)) for lo, hi in ranges]
+        if len(ranges) != len(src.dims):
+            raise GridError(f"ranges has {len(ranges)} axes, grid has {len(src.dims)}")
+        for (lo, hi), n in zip(ranges, src.dims):
+            if lo < 0 or hi > n:
+                raise GridError(f"range ({lo}, {hi}) outside an axis of extent {n}")
+        if any(hi <= lo for lo, hi in ranges):
+            return                                   # empty box: nothing computed or counted
+        with Plan(spec, tuple(src.dims), arith=arith, k=1, kernel="generic") as p:
+            p.upload(box)
+            p.step_box(ranges)
+            out = p.download()
+        sel = tuple(slice(lo, hi) for lo, hi in ranges)
+        sel_box = tuple(slice(r + lo, r + hi) for lo, hi in ranges)
+        interior_view(dst)[sel] = out[sel_box]
+        pts = int(np.prod([hi - lo for lo, hi in ranges]))
+    else:
+        with Plan(spec, tuple(src.dims), arith=arith, k=1) as p:
+            p.upload(box)
+            p.run(1)
+            out = p.download()
+        interior_view(dst)[...] = out[tuple(slice(r, s - r) for s in out.shape)]
         pts = _points(src)
+    if counters is not None:
         counters.point_updates += pts
         counters.scalar_loads += len(spec.weights) * pts
         counters.scalar_stores += pts

@@ -156,6 +156,16 @@ class Plan:
         return Timing(t.device_ms, t.kernel_ms, t.launches, t.point_updates, t.k_used,
                       t.kernel_name.decode())
 
+    def step_box(self, ranges) -> None:
+        """One step over the interior sub-box ``ranges`` = [(lo, hi)] per axis
+        (the reference's ``scalar_step(..., ranges=...)``); only that box of
+        the new current buffer is valid."""
+        if len(ranges) != self.d:
+            raise _abi.GridError(f"ranges has {len(ranges)} axes, grid has {self.d}")
+        lo = (ctypes.c_int64 * 3)(*[int(r[0]) for r in ranges], *([0] * (3 - self.d)))
+        hi = (ctypes.c_int64 * 3)(*[int(r[1]) for r in ranges], *([0] * (3 - self.d)))
+        _abi.check(self._lib.sb_step_box(self._h, lo, hi))
+
     def launch(self, steps: int) -> None:
         _abi.check(self._lib.sb_launch(self._h, int(steps)))
 

@@ -25,13 +25,75 @@ def test_register_into_methods_registry():
     assert methods["b200"] == (Layout.NATURAL, b200_step)
 
 
-def test_step_rejects_aliasing_and_ranges():
+def test_step_rejects_aliasing_and_bad_ranges():
     spec = make_stencil_spec("1d3p")
     g = alloc_grid(spec, 16)
     with pytest.raises(GridError, match="out-of-place"):
         b200_step(g, g, spec)
-    with pytest.raises(GridError, match="ranges"):
-        b200_step(g, alloc_like(g), spec, ranges=[(0, 4)])
+    with pytest.raises(GridError, match="outside"):
+        b200_step(g, alloc_like(g), spec, ranges=[(0, 17)])
+    with pytest.raises(GridError, match="axes"):
+        b200_step(g, alloc_like(g), spec, ranges=[(0, 4), (0, 4)])
+    c = Counters()
+    b200_step(g, alloc_like(g), spec, c, ranges=[(5, 5)])    # empty box: no work, no count
+    assert c.point_updates == 0
+
+
+def _oracle_step(spec, src):
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(np.ascontiguousarray(compact_view(src)), spec.r, offs, ws, 1)
+    r = spec.r
+    return want[tuple(slice(r, s - r) for s in want.shape)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("preset,dims,ranges", [
+    ("1d5p", (1000,), [(17, 403)]),
+    ("2d9p", (41, 66), [(3, 40), (0, 9)]),
+    ("2d5p", (40, 70), [(0, 40), (33, 70)]),
+    ("3d27p", (9, 20, 33), [(2, 7), (5, 6), (1, 32)]),
+    ("3d7p", (8, 21, 30), [(0, 8), (0, 21), (0, 30)]),
+])
+def test_step_ranges_writes_only_the_box(preset, dims, ranges):
+    # scalar_step(..., ranges=...) semantics (kernels.py:88-134)
+    spec = make_stencil_spec(preset)
+    src = alloc_grid(spec, dims)
+    src.set_interior(np.random.default_rng(7).random(dims))
+    dst = alloc_like(src)
+    dst.set_interior(np.full(dims, -7.0))
+    c = Counters()
+    b200_step(src, dst, spec, c, ranges=ranges)
+    got = dst.natural_interior()
+    want = _oracle_step(spec, src)
+    sel = tuple(slice(lo, hi) for lo, hi in ranges)
+    assert np.array_equal(got[sel], want[sel])
+    outside = np.ones(dims, bool)
+    outside[sel] = False
+    assert np.all(got[outside] == -7.0)
+    assert c.point_updates == int(np.prod([hi - lo for lo, hi in ranges]))
+
+
+@pytest.mark.gpu
+def test_tiled_steps_cover_exactly_once():
+    # a tile runner in the reference's style (tiling.py:353-354): disjoint
+    # ranges covering the interior, T ping-pong steps -> the untiled result
+    spec = config_spec("c3b")
+    dims = (37, 50)
+    a = alloc_grid(spec, dims)
+    a.set_interior(np.random.default_rng(3).random(dims))
+    b = alloc_like(a)
+    start = a.natural_interior().copy()
+    tiles = [[(0, 12), (0, 20)], [(0, 12), (20, 50)], [(12, 37), (0, 7)], [(12, 37), (7, 50)]]
+    c = Counters()
+    for _ in range(3):
+        for t in tiles:
+            b200_step(a, b, spec, c, ranges=t)
+        a, b = b, a
+    assert c.point_updates == 3 * 37 * 50
+    ref = alloc_grid(spec, dims)
+    ref.set_interior(start)
+    b200_sweep(ref, spec, 1, 3)
+    assert np.array_equal(a.natural_interior(), ref.natural_interior())
 
 
 @pytest.mark.gpu
