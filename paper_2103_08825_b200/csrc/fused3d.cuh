@@ -289,17 +289,22 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         const int xc = x0 - (K - 1), yc = y0 - (K - 1);         // computed region origin
         // per-thread masks of its 8 points outside the x/y interior / on the halo shell,
         // and their in-plane offsets (for the Dirichlet values)
-        unsigned out_mask = 0, shell_mask = 0;
+        // and the points this thread stores at level K (inside the output tile and the grid)
+        unsigned out_mask = 0, shell_mask = 0, store_mask = 0;
         int64_t hoff[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int y = yc + 4 * ty + (q >> 1), x = xc + 2 * tx + (q & 1);
             const bool out = x < 0 || x >= P.nx || y < 0 || y >= P.ny;
             const bool shell = x >= -1 && x <= P.nx && y >= -1 && y <= P.ny;
+            const int ri = y - y0, cj = x - x0;
+            const bool st = ri >= 0 && ri < TL::TYO && cj >= 0 && cj < TL::TXO && !out;
             out_mask |= (unsigned)out << q;
             shell_mask |= (unsigned)shell << q;
+            store_mask |= (unsigned)st << q;
             hoff[q] = P.origin + (int64_t)y * P.sy + x;
         }
+        T* const obase = P.dst + hoff[0];      // point (0, 0) of this thread; + zc * sz per plane
         int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);      // output planes
         // slab sides: the first/last segment also produces nothing below 0 / above nz
         const int p_first = zs0 - K;
@@ -363,19 +368,14 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                     for (int i = 0; i < 4; i++)
 #pragma unroll
                         for (int j = 0; j < 2; j++) o[(4 * ty + i + 1) * F3_PW + 2 * tx + j + 1] = done[i][j];
-                } else if (zc >= zs0 && zc < zs1) {
+                } else if (zc >= zs0 && zc < zs1 && store_mask) {
+                    T* row = obase + (int64_t)zc * P.sz;
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        const int ri = 4 * ty + i - (K - 1);
-                        const int y = y0 + ri;
-                        if (ri < 0 || ri >= TL::TYO || y >= P.ny) continue;
 #pragma unroll
-                        for (int j = 0; j < 2; j++) {
-                            const int cj = 2 * tx + j - (K - 1);
-                            const int x = x0 + cj;
-                            if (SB_F3_DEBUG != 3 && cj >= 0 && cj < TL::TXO && x >= 0 && x < P.nx)
-                                P.dst[P.origin + (int64_t)zc * P.sz + (int64_t)y * P.sy + x] = done[i][j];
-                        }
+                        for (int j = 0; j < 2; j++)
+                            if ((store_mask >> (2 * i + j)) & 1) row[j] = done[i][j];
+                        row += P.sy;
                     }
                 }
                 if (l < K || K == 1) __syncthreads();

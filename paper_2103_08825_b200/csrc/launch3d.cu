@@ -157,6 +157,9 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
     static const int use_ws = (int)env_double("SB200_3D_WS", 0);
     if (K == 2 && use_ws) return launch_fused3d_ws<T, BOX, FMA>(P, src_idx);
     static const int geo = (int)env_double("SB200_3D_GEO", -1);
+    // 2: 128-thread CTAs, 3 per SM (up to 168 registers: no rematerialised
+    // addressing at K >= 2; measured C4 k=2 348 -> 462, C5 fp64 k=3 269 -> 329)
+    if (geo == 2 || (geo < 0 && sizeof(T) == 8 && K >= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 3>(P, src_idx);
     if (geo == 1 || (geo < 0 && K <= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 4>(P, src_idx);
     return launch_fused3d_g<T, BOX, K, FMA, 8, 2>(P, src_idx);
 }

@@ -123,7 +123,7 @@ int largest_fused_k(int kind, int64_t steps, int kmax) {
 }
 
 int default_k(int kind, const sb_plan* P) {
-    if (kind == KK_FUSED3D) return P->shape == SB_BOX ? 2 : 4;
+    if (kind == KK_FUSED3D) return 2;   // measured best for both 3D stencils (C4, C5)
     if (kind == KK_FUSED2D) return 4;   // measured best on C3 (k=4: ~800, k=8: ~710 GStencil/s)
     // 1D: the deepest composed depth in FMA mode (C2 k=32: ~3960 vs k=16: ~3670;
     // C1 k=64: one launch for T=64), else the level-by-level kernel's 16
