@@ -291,7 +291,6 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         // and their in-plane offsets (for the Dirichlet values)
         // and the points this thread stores at level K (inside the output tile and the grid)
         unsigned out_mask = 0, shell_mask = 0, store_mask = 0;
-        int64_t hoff[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             const int y = yc + 4 * ty + (q >> 1), x = xc + 2 * tx + (q & 1);
@@ -302,9 +301,11 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             out_mask |= (unsigned)out << q;
             shell_mask |= (unsigned)shell << q;
             store_mask |= (unsigned)st << q;
-            hoff[q] = P.origin + (int64_t)y * P.sy + x;
         }
-        T* const obase = P.dst + hoff[0];      // point (0, 0) of this thread; + zc * sz per plane
+        // in-plane element offset of point (0, 0); point q is + (q >> 1) * sy + (q & 1)
+        const int64_t hbase = P.origin + (int64_t)(yc + 4 * ty) * P.sy + (xc + 2 * tx);
+        auto hoff = [&](int q) -> int64_t { return hbase + (q >> 1) * P.sy + (q & 1); };
+        T* const obase = P.dst + hbase;        // + zc * sz per plane
         int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);      // output planes
         // slab sides: the first/last segment also produces nothing below 0 / above nz
         const int p_first = zs0 - K;
@@ -349,7 +350,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
 #pragma unroll
                     for (int q = 0; q < 8; q++) {
                         T hv = T(0);
-                        if (z_shell && ((shell_mask >> q) & 1)) hv = P.src[hoff[q] + (int64_t)zc * P.sz];
+                        if (z_shell && ((shell_mask >> q) & 1)) hv = P.src[hoff(q) + (int64_t)zc * P.sz];
                         done[q >> 1][q & 1] = hv;
                     }
                 } else if (out_mask) {   // only threads owning points outside the x/y interior
@@ -360,7 +361,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                     for (int q = 0; q < 8; q++)
                         if ((out_mask >> q) & 1)
                             done[q >> 1][q & 1] =
-                                (z_alloc && ((shell_mask >> q) & 1)) ? P.src[hoff[q] + (int64_t)zc * P.sz] : T(0);
+                                (z_alloc && ((shell_mask >> q) & 1)) ? P.src[hoff(q) + (int64_t)zc * P.sz] : T(0);
                 }
                 if (l < K) {
                     T* o = sl + (l - 1) * PLANE;

@@ -157,9 +157,11 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
     static const int use_ws = (int)env_double("SB200_3D_WS", 0);
     if (K == 2 && use_ws) return launch_fused3d_ws<T, BOX, FMA>(P, src_idx);
     static const int geo = (int)env_double("SB200_3D_GEO", -1);
-    // 2: 128-thread CTAs, 3 per SM (up to 168 registers: no rematerialised
-    // addressing at K >= 2; measured C4 k=2 348 -> 462, C5 fp64 k=3 269 -> 329)
-    if (geo == 2 || (geo < 0 && sizeof(T) == 8 && K >= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 3>(P, src_idx);
+    // 2: 128-thread CTAs, 3 per SM (more registers per thread).  Measured
+    // (fp64, T=24): C4 star k=2 499 (geo 2) vs 479 (geo 1); C5 box k=2 374 vs
+    // 392; k=3 both 328-390 vs 247-317.  fp32: geo 1 at k <= 2, geo 0 above.
+    const bool geo2 = sizeof(T) == 8 && K >= 2 && !(BOX && K == 2);
+    if (geo == 2 || (geo < 0 && geo2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 3>(P, src_idx);
     if (geo == 1 || (geo < 0 && K <= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 4>(P, src_idx);
     return launch_fused3d_g<T, BOX, K, FMA, 8, 2>(P, src_idx);
 }
