@@ -55,6 +55,7 @@ struct Fused2DParams {
     const Item2D* sched;
     int total_warps;
     unsigned int* counter;   // [0] next item, [1] retired warps
+    unsigned long long* trace;   // debug (SB200_TRACE): per item {smid|warp, t0, t1, strip|rows}
     T w[9];                  // w[(dy+1)*3 + (dx+1)]; star uses 5 entries
 };
 
@@ -126,7 +127,11 @@ fused2d_kernel(const Fused2DParams<T> P) {
     using V = typename Vec16<T>::type;
     extern __shared__ __align__(16) unsigned char smem_f2[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    T* ring = reinterpret_cast<T*>(smem_f2) + warp * F2_DEPTH * F2_ROWW;
+    // ring of RING rows per warp: prefetch distance F2_DEPTH - 1 plus the K
+    // rows already consumed (their x-halo columns are the Dirichlet values of
+    // the rows completed by levels 1..K: no global reload on the edge strips)
+    constexpr int RING = F2_DEPTH + K;
+    T* ring = reinterpret_cast<T*>(smem_f2) + warp * RING * F2_ROWW;
     // shared row layout: [VEC-1] left edge, [VEC..VEC+CW) strip columns, [VEC+CW] right edge
 
     auto claim_issue = [&]() -> unsigned {
@@ -139,6 +144,8 @@ fused2d_kernel(const Fused2DParams<T> P) {
     while (item < (unsigned)P.items) {
         const unsigned next_raw = claim_issue();        // resolved after this item
         const Item2D it = P.sched[item];
+        unsigned long long tr0 = 0;
+        if (P.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         const int x0 = TL::X0 + it.tix * TL::TXO;       // output strip origin
         const int xc = x0 - TL::HL;                     // computed strip origin (16 B aligned)
         const int ys0 = it.ys0, ys1 = it.ys1;
@@ -164,7 +171,7 @@ fused2d_kernel(const Fused2DParams<T> P) {
         const bool eload = (lane == 0 || lane == 31) && ecol >= -1 && ecol <= P.nx;
 
         auto stage = [&](int t) {
-            T* row = ring + (t % F2_DEPTH) * F2_ROWW;
+            T* row = ring + (t % RING) * F2_ROWW;
             const int y = p_first + t;
             const bool rok = t < M && y >= P.row_lo && y < P.row_hi;
             const T* g = P.src + P.origin + (int64_t)y * P.sy;
@@ -192,12 +199,12 @@ fused2d_kernel(const Fused2DParams<T> P) {
         for (int t = 0; t < M; t++) {
             cp_async_wait<F2_DEPTH - 2>();
             __syncwarp();
-            const T* row = ring + (t % F2_DEPTH) * F2_ROWW;
+            const T* row = ring + (t % RING) * F2_ROWW;
             T v[F2_VX];
 #pragma unroll
             for (int j = 0; j < F2_VX; j++) v[j] = row[VEC + F2_VX * lane + j];
             T edge = lane == 0 ? row[VEC - 1] : row[VEC + F2_CW];
-            __syncwarp();                                   // slot t-1 fully read before restaging
+            __syncwarp();                                   // slot t-K-1 fully read before restaging
             stage(t + F2_DEPTH - 1);
             const int a0 = p_first + t;
             // no level of this row touches a physical y halo and the strip no x halo
@@ -217,19 +224,21 @@ fused2d_kernel(const Fused2DParams<T> P) {
                 f2_push<T, BOX, FMA>(u, Pm[l - 1], P0[l - 1], done, P.w);
                 const int yc = a0 - l;                      // completed level-l row
                 const bool y_out = yc < ylo || yc >= yhi;
-                if (!plain && (y_out || warp_out)) {        // (warp-uniform) Dirichlet halo, same at every level
+                if (!plain && y_out) {                      // (warp-uniform) physical y-halo row
                     const bool y_shell = yc >= -1 && yc <= P.ny;
                     const bool y_alloc = yc >= P.row_lo && yc < P.row_hi;
                     const T* rowp = P.src + P.origin + (int64_t)yc * P.sy;
 #pragma unroll
                     for (int j = 0; j < F2_VX; j++) {
-                        if (y_out || ((out_mask >> j) & 1)) {
-                            // the y-shell test applies only to physical halo rows; ghost rows
-                            // are real grid rows whose x-halo cells are Dirichlet
-                            const bool sh = y_alloc && (!y_out || y_shell) && ((shell_mask >> j) & 1);
-                            done[j] = sh ? rowp[col[j]] : T(0);
-                        }
+                        const bool sh = y_alloc && y_shell && ((shell_mask >> j) & 1);
+                        done[j] = sh ? rowp[col[j]] : T(0);
                     }
+                } else if (warp_out) {                      // x-halo columns of an interior (or ghost) row:
+                    // the level-0 value of row yc, still in the ring (zero-filled outside the allocation)
+                    const T* r0 = ring + ((t - l + RING) % RING) * F2_ROWW + VEC + F2_VX * lane;
+#pragma unroll
+                    for (int j = 0; j < F2_VX; j++)
+                        if ((out_mask >> j) & 1) done[j] = ((shell_mask >> j) & 1) ? r0[j] : T(0);
                 }
                 if (l < K) {
 #pragma unroll
@@ -254,6 +263,16 @@ fused2d_kernel(const Fused2DParams<T> P) {
         }
         cp_async_wait<0>();
         __syncwarp();
+        if (P.trace && lane == 0) {
+            unsigned long long tr1;
+            unsigned smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            P.trace[4 * item + 0] = ((unsigned long long)smid << 32) | (blockIdx.x * F2_WARPS + warp);
+            P.trace[4 * item + 1] = tr0;
+            P.trace[4 * item + 2] = tr1;
+            P.trace[4 * item + 3] = ((unsigned long long)it.tix << 40) | (unsigned long long)(it.ys1 - it.ys0);
+        }
         item = __shfl_sync(0xffffffffu, next_raw, 0);
     }
     if (lane == 0) {
@@ -265,7 +284,7 @@ fused2d_kernel(const Fused2DParams<T> P) {
     }
 }
 
-template <typename T>
-constexpr int fused2d_smem_bytes() { return F2_WARPS * F2_DEPTH * F2_ROWW * (int)sizeof(T); }
+template <typename T, int K>
+constexpr int fused2d_smem_bytes() { return F2_WARPS * (F2_DEPTH + K) * F2_ROWW * (int)sizeof(T); }
 
 }  // namespace sb

@@ -20,7 +20,9 @@ std::vector<sb::Item2D> guided_schedule_2d(int tiles_x, int64_t ny, int64_t warp
     std::vector<sb::Item2D> out;
     std::vector<int64_t> pos(tiles_x, 0);   // per-strip cursor
     const int64_t total = (int64_t)tiles_x * ny;
-    const int64_t per_strip = std::max<int64_t>(1, (warps + tiles_x - 1) / tiles_x);
+    // about one item per warp per round, never more items than warps (a first-round
+    // item left over for a late claim is a long tail: traced on C3)
+    const int64_t per_strip = std::max<int64_t>(1, warps / tiles_x);
     int64_t done = 0;
     bool first = true;
     while (done < total) {
@@ -51,7 +53,7 @@ template <typename T, bool BOX, int K, bool FMA>
 int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     using TL = sb::F2Tile<T, K>;
     auto kern = sb::fused2d_kernel<T, BOX, K, FMA>;
-    const int smem = sb::fused2d_smem_bytes<T>();
+    const int smem = sb::fused2d_smem_bytes<T, K>();
     Sched1D* sc = nullptr;
     for (auto& e : P->sched1d)
         if (e.K == 1000 + K) sc = &e;   // 2D schedules keyed by 1000 + K
@@ -86,6 +88,12 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     const int blocks = std::min(sc->blocks, (prm.items + sb::F2_WARPS - 1) / sb::F2_WARPS);
     prm.total_warps = blocks * sb::F2_WARPS;
     prm.counter = P->d_counter;
+    prm.trace = nullptr;
+    if (getenv("SB200_TRACE")) {   // debug: per-item trace of the last launch (sb_run writes it out)
+        if (!P->d_trace) SB_CUDA(cudaMalloc(&P->d_trace, sizeof(unsigned long long) * 4 * (1 << 20)));
+        if (prm.items <= (1 << 20)) prm.trace = P->d_trace;
+        P->trace_n = prm.items;
+    }
     for (int i = 0; i < 9; i++) prm.w[i] = T(0);
     for (int i = 0; i < P->nw; i++) {
         const int* o = &P->offsets[2 * i];
