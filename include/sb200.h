@@ -17,6 +17,9 @@
  *   sb_download      <- GridBuffer.natural_interior (core.py:308-316)
  *   sb_step_box      <- scalar_step(..., ranges=...) as driven by the tiled
  *                       runner (tiling.py:353-354)
+ *   sb_upload_storage / sb_download_storage / sb_layout_convert
+ *                    <- the layout conversions of transpose.py:266-357
+ *                       (BLOCK_TRANSPOSE / DLT storage), see below
  *   sb_upload_async / sb_download_async / sb_synchronize
  *                    <- (no reference counterpart: stream-ordered transfers
  *                       for overlapping independent grids' sweeps)
@@ -144,6 +147,43 @@ int sb_set_stream(sb_plan *plan, void *cuda_stream);
  * interior point (0,...,0); strides[0..d-1] in elements. */
 int sb_device_view(const sb_plan *plan, int which, void **base,
                    int64_t *origin, int64_t strides[3]);
+
+/* ---- reference storage layouts (stencilbench/transpose.py, core.py:206-229)
+ *
+ * A reference GridBuffer stores each unit-stride row as
+ * [halo_unit | unit_np padded region | halo_unit] (halo_unit = 2r,
+ * core.py:35, 260-266); the padded region is NATURAL, BLOCK_TRANSPOSE (every
+ * vl x vl block transposed) or DLT (the region viewed as vl x unit_np/vl and
+ * transposed).  Cells in [unit_n, unit_np) are Dirichlet padding. */
+typedef enum { SB_LAYOUT_NATURAL = 0, SB_LAYOUT_BLOCK_TRANSPOSE = 1, SB_LAYOUT_DLT = 2 } sb_layout;
+
+typedef struct sb_storage {
+    int32_t layout;          /* sb_layout */
+    int32_t vl;              /* 4 or 8 (SUPPORTED_VL, core.py:31); ignored for NATURAL */
+    int64_t unit_n;          /* interior unit-stride extent */
+    int64_t unit_np;         /* padded extent: multiple of vl*vl (BLOCK_TRANSPOSE) / vl (DLT) */
+    int64_t halo_unit;       /* unit-axis halo cells per side (>= r; the reference uses 2r) */
+} sb_storage;
+
+/* Whole reference storage array (GridBuffer.data: rows of unit_np +
+ * 2*halo_unit elements, outer axes with their r halo rows, C order) in layout
+ * st -> the plan, un-permuted on the device.  Replaces the host-side
+ * from_block_transpose / from_dlt + natural_interior path (transpose.py:
+ * 303-311, 338-357) of a caller holding a BLOCK_TRANSPOSE or DLT grid (e.g.
+ * jam_sweep's, timejam.py:288-304).  Whole-grid plans only. */
+int sb_upload_storage(sb_plan *plan, const void *host, size_t bytes, const sb_storage *st);
+/* The plan's current grid -> the same storage array, re-permuted on the
+ * device into layout st; every cell that is not an interior point keeps the
+ * value of the last sb_upload_storage (required first, same geometry). */
+int sb_download_storage(sb_plan *plan, void *host, size_t bytes, const sb_storage *st);
+/* Device-to-device conversion of `rows` storage rows (unit_np + 2*halo_unit
+ * elements each, dtype sb_dtype): to_layout != 0 converts NATURAL `src` to
+ * layout st->layout in `dst` (to_block_transpose / to_dlt, transpose.py:
+ * 286-301, 314-336); to_layout == 0 is the inverse (from_block_transpose /
+ * from_dlt).  Out-of-place, asynchronous on `stream` (NULL = legacy default
+ * stream); halo cells are copied unchanged. */
+int sb_layout_convert(void *dst, const void *src, int64_t rows, const sb_storage *st, int32_t to_layout,
+                      int32_t dtype, void *stream);
 
 /* Fused depth the plan will use per launch. */
 int sb_plan_k(const sb_plan *plan, int32_t *k);

@@ -17,12 +17,14 @@ SB_F64, SB_F32 = 0, 1
 SB_ARITH_EXACT, SB_ARITH_FMA = 0, 1
 SB_STAR, SB_BOX = 0, 1
 SB_KERNEL_AUTO, SB_KERNEL_GENERIC, SB_KERNEL_FUSED = 0, 1, 2
+SB_LAYOUT_NATURAL, SB_LAYOUT_BLOCK_TRANSPOSE, SB_LAYOUT_DLT = 0, 1, 2
 
 #: every symbol include/sb200.h declares (checked by tests/test_abi.py)
 EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_download", "sb_run", "sb_launch", "sb_set_stream", "sb_device_view",
            "sb_plan_k", "sb_kernel_count", "sb_last_error", "sb_abi_version", "sb_device_count",
-           "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box")
+           "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
+           "sb_upload_storage", "sb_download_storage", "sb_layout_convert")
 
 
 class SbProblem(ctypes.Structure):
@@ -41,6 +43,11 @@ class SbTiming(ctypes.Structure):
                 ("launches", ctypes.c_int64), ("point_updates", ctypes.c_int64),
                 ("k_used", ctypes.c_int32), ("reserved", ctypes.c_int32),
                 ("kernel_name", ctypes.c_char * 64)]
+
+
+class SbStorage(ctypes.Structure):
+    _fields_ = [("layout", ctypes.c_int32), ("vl", ctypes.c_int32), ("unit_n", ctypes.c_int64),
+                ("unit_np", ctypes.c_int64), ("halo_unit", ctypes.c_int64)]
 
 
 class CudaError(RuntimeError):
@@ -77,13 +84,19 @@ def load():
                                    ctypes.POINTER(ctypes.c_int64), ctypes.c_int64 * 3]
     lib.sb_plan_k.argtypes = [P, ctypes.POINTER(ctypes.c_int32)]
     lib.sb_kernel_count.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
+    SP = ctypes.POINTER(SbStorage)
+    lib.sb_upload_storage.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, SP]
+    lib.sb_download_storage.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, SP]
+    lib.sb_layout_convert.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, SP, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.c_void_p]
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_last_error.argtypes = []
     lib.sb_abi_version.restype = ctypes.c_int
     lib.sb_device_count.restype = ctypes.c_int
     for name in ("sb_plan_create", "sb_host_elems", "sb_upload", "sb_download", "sb_run",
                  "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k", "sb_kernel_count",
-                 "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box"):
+                 "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
+                 "sb_upload_storage", "sb_download_storage", "sb_layout_convert"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

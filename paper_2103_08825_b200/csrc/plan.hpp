@@ -89,6 +89,9 @@ struct sb_plan {
     std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
     CUtensorMap tmap[2][2];                // TMA descriptors [geometry][buffer] (3D)
     bool tmap_ok[2] = {false, false};
+    void* stage = nullptr;                 // reference-storage staging rows (sb_upload_storage)
+    size_t stage_bytes = 0;
+    int64_t stage_row_elems = 0;
     unsigned long long* d_trace = nullptr;  // debug trace (SB200_TRACE)
     int trace_n = 0;
     int kind = sbh::KK_GENERIC;
@@ -109,6 +112,7 @@ int launch_fused1d(sb_plan* P, int src_idx, int k);
 int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
 int make_tensor_maps(sb_plan* P, int geo, int box_h);
+int finish_upload(sb_plan* P);   // buf[0] uploaded: mirror halo/ghost into buf[1], make buf[0] current
 
 // The composed 1D path (compose1d.cuh) serves depth k when the arithmetic is
 // FMA, R*k <= 64 taps each side, the halo is a whole number of 16 B vectors

@@ -314,6 +314,12 @@ int enqueue_upload(sb_plan* P, const void* host, size_t bytes) {
     char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
     SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, host, P->host_row_elems * P->es,
                               P->host_row_elems * P->es, P->host_rows, cudaMemcpyHostToDevice, P->stream));
+    return finish_upload(P);
+}
+
+// buf[0] holds the uploaded box: mirror the halo/ghost into buf[1] (kernels
+// never write it) and make buf[0] current.
+int finish_upload(sb_plan* P) {
     if (P->d == 1) {
         const size_t lo = (size_t)P->g.origin, hi = (size_t)(P->g.origin + P->g.n[2]);
         char* b0 = reinterpret_cast<char*>(P->buf[0]);
@@ -367,6 +373,7 @@ void sb_plan_destroy(sb_plan* P) {
     if (P->d_w) cudaFree(P->d_w);
     if (P->d_counter) cudaFree(P->d_counter);
     if (P->d_trace) cudaFree(P->d_trace);
+    if (P->stage) cudaFree(P->stage);
     for (auto& e : P->sched1d)
         if (e.d_chunks) cudaFree(e.d_chunks);
     for (auto& g : P->graphs)

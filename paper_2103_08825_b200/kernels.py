@@ -11,7 +11,17 @@ kernels:
   read-only, EXACT arithmetic: bit-identical to ``scalar_step``);
 * :func:`b200_sweep` -- jam_sweep-compatible T-step in-place sweep with k
   fused steps per HBM round trip (any k the fused kernel supports);
-* :func:`register` -- adds ``"b200"`` to a reference ``METHODS`` registry.
+* :func:`register` -- adds ``"b200"`` (NATURAL) and, when the registry's
+  Layout enum has them, ``"b200_transpose"`` (BLOCK_TRANSPOSE, the layout of
+  the reference's ``"transpose"`` method and of ``jam_sweep``) and
+  ``"b200_dlt"`` (DLT) to a reference ``METHODS`` registry.
+
+Grids in BLOCK_TRANSPOSE or DLT layout travel as whole storage arrays and are
+permuted to and from the natural order on the device (``sb_upload_storage``
+/ ``sb_download_storage``, ``csrc/layout.cuh``); the sweep itself always runs
+the natural-order kernels, so results are bit-identical to the reference's
+``transpose_layout_step`` / ``dlt_step`` / ``jam_sweep`` (which are
+bit-identical to ``scalar_step``, test_kernels.py:82, test_timejam.py:94).
 """
 
 from __future__ import annotations
@@ -19,7 +29,7 @@ from __future__ import annotations
 import numpy as np
 
 from .core import GridError, validate
-from .grid import compact_view, interior_view, is_natural
+from .grid import compact_view, interior_view, is_natural, layout_value, unit_permutation
 from .plan import Plan
 
 
@@ -27,9 +37,10 @@ def _check_pair(src, dst) -> None:
     # kernels.py:111-117
     if src is dst:
         raise GridError("single steps are out-of-place: src and dst must differ")
-    if not (is_natural(src) and is_natural(dst)):
-        raise GridError("method requires natural layout on both grids")
-    if tuple(src.dims) != tuple(dst.dims) or src.unit_np != dst.unit_np:
+    if layout_value(src) != layout_value(dst):
+        raise GridError("src and dst grids have different layouts")
+    if tuple(src.dims) != tuple(dst.dims) or src.unit_np != dst.unit_np or \
+            getattr(src, "vl", 4) != getattr(dst, "vl", 4):
         raise GridError("src and dst grids have mismatched geometry")
 
 
@@ -40,6 +51,28 @@ def _points(grid) -> int:
     return n
 
 
+def _check_ranges(ranges, dims):
+    ranges = [(int(lo), int(hi)) for lo, hi in ranges]
+    if len(ranges) != len(dims):
+        raise GridError(f"ranges has {len(ranges)} axes, grid has {len(dims)}")
+    for (lo, hi), n in zip(ranges, dims):
+        if lo < 0 or hi > n:
+            raise GridError(f"range ({lo}, {hi}) outside an axis of extent {n}")
+    return ranges
+
+
+def _store_interior(dst, storage: np.ndarray, ranges=None) -> None:
+    """Copy the interior (or the ``ranges`` box) of a storage array in dst's
+    layout into ``dst.data``; everything else of dst stays as it was."""
+    hu = dst.halo_unit
+    perm = unit_permutation(layout_value(dst), dst.unit_np, getattr(dst, "vl", 4))
+    if ranges is None:
+        ranges = [(0, n) for n in dst.dims]
+    outer = tuple(slice(dst.r + lo, dst.r + hi) for lo, hi in ranges[:-1])
+    cols = hu + perm[ranges[-1][0]:ranges[-1][1]]
+    dst.data[outer + (cols,)] = storage[outer + (cols,)]
+
+
 def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> None:
     """One sweep ``dst = S(src)`` on the GPU (signature of kernels.py:120-134).
 
@@ -47,35 +80,37 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
     sub-box, as the reference's tiled runner drives it (tiling.py:353-354):
     the device computes only the box (sb_step_box) and only the box of
     ``dst`` is written; counters count the box's points (kernels.py:127-134).
+    Grids may be NATURAL, BLOCK_TRANSPOSE or DLT (both in the same layout).
     """
     _check_pair(src, dst)
     validate(spec)
     r = spec.r
-    box = np.ascontiguousarray(compact_view(src), dtype=np.float64)
+    natural = is_natural(src)
     if ranges is not None:
-        ranges = [(int(lo), int(hi)) for lo, hi in ranges]
-        if len(ranges) != len(src.dims):
-            raise GridError(f"ranges has {len(ranges)} axes, grid has {len(src.dims)}")
-        for (lo, hi), n in zip(ranges, src.dims):
-            if lo < 0 or hi > n:
-                raise GridError(f"range ({lo}, {hi}) outside an axis of extent {n}")
+        ranges = _check_ranges(ranges, src.dims)
         if any(hi <= lo for lo, hi in ranges):
             return                                   # empty box: nothing computed or counted
-        with Plan(spec, tuple(src.dims), arith=arith, k=1, kernel="generic") as p:
-            p.upload(box)
+    kernel = "generic" if ranges is not None else "auto"
+    with Plan(spec, tuple(src.dims), arith=arith, k=1, kernel=kernel) as p:
+        if natural:
+            p.upload(np.ascontiguousarray(compact_view(src), dtype=np.float64))
+        else:
+            p.upload_storage(src)
+        if ranges is not None:
             p.step_box(ranges)
-            out = p.download()
-        sel = tuple(slice(lo, hi) for lo, hi in ranges)
-        sel_box = tuple(slice(r + lo, r + hi) for lo, hi in ranges)
-        interior_view(dst)[sel] = out[sel_box]
-        pts = int(np.prod([hi - lo for lo, hi in ranges]))
-    else:
-        with Plan(spec, tuple(src.dims), arith=arith, k=1) as p:
-            p.upload(box)
+        else:
             p.run(1)
-            out = p.download()
-        interior_view(dst)[...] = out[tuple(slice(r, s - r) for s in out.shape)]
-        pts = _points(src)
+        out = p.download() if natural else p.download_storage(src)
+    if natural:
+        if ranges is None:
+            interior_view(dst)[...] = out[tuple(slice(r, s - r) for s in out.shape)]
+        else:
+            sel = tuple(slice(lo, hi) for lo, hi in ranges)
+            sel_box = tuple(slice(r + lo, r + hi) for lo, hi in ranges)
+            interior_view(dst)[sel] = out[sel_box]
+    else:
+        _store_interior(dst, out, ranges)
+    pts = _points(src) if ranges is None else int(np.prod([hi - lo for lo, hi in ranges]))
     if counters is not None:
         counters.point_updates += pts
         counters.scalar_loads += len(spec.weights) * pts
@@ -85,25 +120,43 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
 def b200_sweep(grid, spec, k, T, counters=None, *, arith="exact") -> None:
     """Advance ``grid`` T steps in place, k fused steps per launch (timejam.py:288-304).
 
-    Unlike the reference register pipeline (k in {1, 2}, 1D, r <= 2), any
-    dimension and any k in {1, 2, 4, 8, 16} is accepted; T need not be a
+    Unlike the reference register pipeline (k in {1, 2}, 1D, r <= 2,
+    BLOCK_TRANSPOSE only), any dimension, layout (NATURAL, BLOCK_TRANSPOSE,
+    DLT) and any k the fused kernels support is accepted; T need not be a
     multiple of k (the tail runs at smaller k).
     """
-    if not is_natural(grid):
-        raise GridError("b200 sweep runs on natural-layout grids")
     validate(spec)
     if T < 0:
         raise GridError(f"total steps T={T} must be >= 0")
-    box = np.ascontiguousarray(compact_view(grid), dtype=np.float64)
+    natural = is_natural(grid)
     with Plan(spec, tuple(grid.dims), arith=arith, k=k) as p:
-        p.upload(box)
+        if natural:
+            p.upload(np.ascontiguousarray(compact_view(grid), dtype=np.float64))
+        else:
+            p.upload_storage(grid)
         p.run(T)
-        out = p.download()
-    interior_view(grid)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
+        if natural:
+            out = p.download()
+            interior_view(grid)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
+        else:
+            out = p.download_storage(grid)
+            _store_interior(grid, out)
     if counters is not None:
         counters.point_updates += _points(grid) * T
 
 
-def register(methods: dict, natural_layout) -> None:
-    """Register ``"b200"`` in a reference METHODS dict (kernels.py:538-544)."""
-    methods["b200"] = (natural_layout, b200_step)
+def register(methods: dict, layout) -> None:
+    """Register the b200 methods in a reference METHODS dict (kernels.py:538-544).
+
+    ``layout`` is the registry's Layout enum (or any of its members, e.g.
+    ``Layout.NATURAL`` as in ``register(METHODS, Layout.NATURAL)``).
+    """
+    enum = layout if isinstance(layout, type) else type(layout)
+    methods["b200"] = (getattr(enum, "NATURAL", layout), b200_step)
+    if hasattr(enum, "BLOCK_TRANSPOSE"):
+        methods["b200_transpose"] = (enum.BLOCK_TRANSPOSE, b200_step)
+    if hasattr(enum, "DLT"):
+        methods["b200_dlt"] = (enum.DLT, b200_step)
+
+
+__all__ = ["b200_step", "b200_sweep", "register"]

@@ -146,6 +146,28 @@ class Plan:
         _abi.check(self._lib.sb_download_async(self._h, out.ctypes.data, out.nbytes))
         return out
 
+    def upload_storage(self, grid) -> None:
+        """Upload a reference-storage grid (``GridBuffer.data`` in NATURAL,
+        BLOCK_TRANSPOSE or DLT layout, any vl) and un-permute it on the device."""
+        data, st = self._storage(grid)
+        _abi.check(self._lib.sb_upload_storage(self._h, data.ctypes.data, data.nbytes, ctypes.byref(st)))
+
+    def download_storage(self, grid, out: np.ndarray | None = None) -> np.ndarray:
+        """The current grid, permuted on the device into ``grid``'s layout, as a
+        full storage array (default: a new array shaped like ``grid.data``);
+        non-interior cells keep the values of the last :meth:`upload_storage`."""
+        data, st = self._storage(grid)
+        if out is None:
+            out = np.empty_like(data)
+        if out.shape != data.shape or out.dtype != data.dtype or not out.flags.c_contiguous:
+            raise GridError("storage output must match the grid's storage array")
+        _abi.check(self._lib.sb_download_storage(self._h, out.ctypes.data, out.nbytes, ctypes.byref(st)))
+        return out
+
+    def _storage(self, grid):
+        data = np.ascontiguousarray(grid.data, dtype=self.np_dtype)
+        return data, storage_descriptor(grid)
+
     def synchronize(self) -> None:
         _abi.check(self._lib.sb_synchronize(self._h))
 
@@ -188,6 +210,22 @@ class Plan:
         return int(base.value or 0), int(origin.value), tuple(strides[: self.d])
 
 
+_LAYOUT_CODES = {"natural": _abi.SB_LAYOUT_NATURAL, "block_transpose": _abi.SB_LAYOUT_BLOCK_TRANSPOSE,
+                 "dlt": _abi.SB_LAYOUT_DLT}
+
+
+def storage_descriptor(grid) -> _abi.SbStorage:
+    """C-ABI ``sb_storage`` of a (reference or sb200) GridBuffer."""
+    from .grid import layout_value
+    st = _abi.SbStorage()
+    st.layout = _LAYOUT_CODES[layout_value(grid)]
+    st.vl = int(getattr(grid, "vl", 4))
+    st.unit_n = int(grid.unit_n)
+    st.unit_np = int(grid.unit_np)
+    st.halo_unit = int(grid.halo_unit)
+    return st
+
+
 def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
           device=0, dtype=None) -> np.ndarray:
     """``steps`` Jacobi steps of ``spec`` over a compact halo-inclusive ``box``.
@@ -211,4 +249,4 @@ def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
         return p.download()
 
 
-__all__ = ["Plan", "Timing", "sweep", "host_shape", "SpecError", "GridError"]
+__all__ = ["Plan", "Timing", "sweep", "host_shape", "storage_descriptor", "SpecError", "GridError"]

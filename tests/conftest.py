@@ -25,8 +25,11 @@ def pytest_configure(config):
 
 
 def golden_names():
+    """Natural-layout sweep fixtures (make_golden.py); the l_* layout fixtures
+    (make_golden_layouts.py) have their own tests (test_layouts.py)."""
     return sorted(os.path.splitext(os.path.basename(p))[0]
-                  for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz")))
+                  for p in glob.glob(os.path.join(GOLDEN_DIR, "*.npz"))
+                  if not os.path.basename(p).startswith("l_"))
 
 
 def load_golden(name):
