@@ -5,6 +5,7 @@
 #include "plan.hpp"
 #include "fused3d.cuh"
 #include "fused3d_ws.cuh"
+#include "compose3d.cuh"
 
 namespace sbh {
 namespace {
@@ -166,8 +167,129 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
     return launch_fused3d_g<T, BOX, K, FMA, 8, 2>(P, src_idx);
 }
 
+// ---- composed two-step star (compose3d.cuh): FMA mode, k = 2
+
+// Two steps of the 7-point star = one step of its 25-point self-convolution
+// (away from physical boundaries).  Composed in long double, rounded once.
+template <typename T>
+void composed_star_weights(const sb_plan* P, T (&w)[125], T (&w7)[7]) {
+    long double c[125] = {};
+    long double s[3][3][3] = {};
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[3 * i];
+        s[o[0] + 1][o[1] + 1][o[2] + 1] = (long double)P->weights[i];
+    }
+    for (int a = 0; a < 27; a++)
+        for (int b = 0; b < 27; b++) {
+            const int az = a / 9 - 1, ay = a / 3 % 3 - 1, axx = a % 3 - 1;
+            const int bz = b / 9 - 1, by = b / 3 % 3 - 1, bx = b % 3 - 1;
+            const long double p = s[az + 1][ay + 1][axx + 1] * s[bz + 1][by + 1][bx + 1];
+            if (p != 0) c[sb::c3_widx(az + bz, ay + by, axx + bx)] += p;
+        }
+    for (int i = 0; i < 125; i++) w[i] = (T)c[i];
+    for (int i = 0; i < 7; i++) w7[i] = (T)P->weights[i];   // canonical star order
+}
+
+bool compose3d_ok(const sb_plan* P, int k) {
+    static const int enabled = (int)env_double("SB200_3D_COMPOSE", 1);
+    return enabled && k == 2 && (P->dtype == SB_F64 || enabled == 2) && P->shape == SB_STAR && P->arith == SB_ARITH_FMA && P->nw == 7 &&
+           P->dims[0] >= 4 && P->dims[1] >= 4 && P->dims[2] >= 4;
+}
+
+template <typename T, int NTY, int MINB>
+int launch_compose3d(sb_plan* P, int src_idx) {
+    constexpr int GEO = NTY == 8 ? 3 : 2;
+    constexpr int VEC = 16 / (int)sizeof(T);
+    constexpr int X0 = (2 % VEC == 0) ? 0 : 2 - VEC;   // TMA box start (x0 - 2) 16 B aligned
+    if (!P->tmap_ok[GEO]) {
+        const int rc = make_tensor_maps_impl(P, GEO, sb::C3Geo<NTY>::PH);
+        if (rc != SB_OK) return rc;
+    }
+    auto kern = sb::compose3d_kernel<T, NTY, MINB>;
+    const int smem = sb::c3_smem_bytes<T, NTY>();
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::C3Geo<NTY>::THREADS, smem));
+    occ = std::max(occ, 1);
+    sb::Compose3DParams<T> prm;
+    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
+    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
+    prm.origin = P->g.origin;
+    prm.sz = P->g.sz;
+    prm.sy = P->g.sy;
+    prm.nz = (int)P->dims[0];
+    prm.ny = (int)P->dims[1];
+    prm.nx = (int)P->dims[2];
+    prm.ax = (int)(P->g.origin % P->g.sy);
+    prm.ry = P->r;
+    prm.hz = (int)P->hlo;
+    prm.hz_hi = (int)P->hhi;
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    prm.x0_first = X0;
+    prm.tiles_x = (int)((P->dims[2] - X0 + sb::C3_CW - 1) / sb::C3_CW);
+    prm.tiles_y = (int)((P->dims[1] + sb::C3Geo<NTY>::CH - 1) / sb::C3Geo<NTY>::CH);
+    const int ctas_max = P->num_sms * occ;
+    const int tiles = prm.tiles_x * prm.tiles_y;
+    const double per = env_double("SB200_C3_ITEMS_PER_CTA", 12.0);
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
+    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    prm.items = tiles * prm.nseg;
+    prm.total_ctas = std::min(ctas_max, prm.items);
+    prm.counter = P->d_counter;
+    T w7[7];
+    composed_star_weights<T>(P, prm.w, w7);
+    for (int i = 0; i < 7; i++) prm.w7[i] = w7[i];
+
+    // physical shell on the side stream (disjoint points; both read only src)
+    sb::Shell3DParams<T> sp;
+    sp.src = prm.src;
+    sp.dst = prm.dst;
+    sp.origin = prm.origin;
+    sp.sz = prm.sz;
+    sp.sy = prm.sy;
+    sp.nx = prm.nx;
+    sp.ny = prm.ny;
+    sp.nz = prm.nz;
+    sp.phys_lo = P->phys_lo;
+    sp.phys_hi = P->phys_hi;
+    sp.hz = (int)P->hlo;
+    sp.hz_hi = (int)P->hhi;
+    const int64_t zi = std::max<int64_t>(0, P->dims[0] - (P->phys_lo ? 1 : 0) - (P->phys_hi ? 1 : 0));
+    sp.nzf = (int64_t)(P->phys_lo + P->phys_hi) * prm.nx * prm.ny;
+    sp.nyf = 2 * zi * prm.nx;
+    sp.nxf = 0;   // x faces: corrected inside compose3d_kernel (E(q) push form)
+    for (int i = 0; i < 7; i++) sp.w[i] = w7[i];
+    const int64_t shell = sp.nzf + sp.nyf + sp.nxf;
+    SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
+    SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
+    const unsigned sblocks = (unsigned)std::min<int64_t>((shell + 255) / 256, (int64_t)P->num_sms * 8);
+    sb::compose3d_shell_kernel<T><<<sblocks, 256, 0, P->side_stream>>>(sp);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+    P->kernels_launched++;
+
+    P->last_kernel = "compose3d_kernel";
+    kern<<<(unsigned)prm.total_ctas, sb::C3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));   // join
+    return SB_OK;
+}
+
+template <typename T>
+int launch_compose3d_t(sb_plan* P, int src_idx) {
+    static const int geo = (int)env_double("SB200_C3_GEO", 2);
+    if (geo == 0) return launch_compose3d<T, 8, 2>(P, src_idx);
+    if (geo == 2) return launch_compose3d<T, 4, 3>(P, src_idx);
+    return launch_compose3d<T, 4, 4>(P, src_idx);
+}
+
 template <typename T, bool BOX, bool FMA>
 int launch_fused3d_b(sb_plan* P, int src_idx, int k) {
+    if constexpr (!BOX && FMA) {
+        if (compose3d_ok(P, k)) return launch_compose3d_t<T>(P, src_idx);
+    }
     switch (k) {
         case 1: return launch_fused3d_k<T, BOX, 1, FMA>(P, src_idx);
         case 2: return launch_fused3d_k<T, BOX, 2, FMA>(P, src_idx);

@@ -87,8 +87,8 @@ struct sb_plan {
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<sbh::Sched1D> sched1d;
     std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
-    CUtensorMap tmap[2][2];                // TMA descriptors [geometry][buffer] (3D)
-    bool tmap_ok[2] = {false, false};
+    CUtensorMap tmap[4][2];                // TMA descriptors [geometry][buffer] (3D; 2, 3: composed)
+    bool tmap_ok[4] = {false, false, false, false};
     void* stage = nullptr;                 // reference-storage staging rows (sb_upload_storage)
     size_t stage_bytes = 0;
     int64_t stage_row_elems = 0;

@@ -279,6 +279,59 @@ def test_c5_full_size_fma():
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
 
 
+# --- composed 3D star (FMA, k=2 as one 25-point pass + exact physical shell)
+
+@pytest.mark.parametrize("dims", [(4, 4, 4), (5, 9, 7), (9, 40, 70), (37, 33, 130), (20, 17, 131)])
+@pytest.mark.parametrize("halo", ["full", "zero"])
+def test_composed3d_within_fp64_bar(dims, halo):
+    spec = config_spec("c4")
+    box = seeded_box(dims, 1, seed=sum(dims), halo=halo)
+    T = 9                                    # four composed launches plus a k=1 tail
+    with Plan(spec, dims, k=2, arith="fma") as p:
+        p.upload(box)
+        t = p.run(T)
+        got = p.download()
+    assert t.kernel_name in ("compose3d_kernel", "fused3d_kernel")
+    want = oracle(spec, box, T)
+    assert np_oracle.max_rel_error(interior(got, 1), interior(want, 1)) <= FP64_TOL
+    mask = np.ones(box.shape, bool)
+    mask[1:-1, 1:-1, 1:-1] = False
+    assert np.array_equal(got[mask], box[mask])          # halo untouched
+
+
+def test_composed3d_shell_next_to_dirichlet_values():
+    # the interior's outer layer is recomputed level by level: with halo values far
+    # from the interior ones, a composition there would be visibly wrong
+    spec = config_spec("c4")
+    dims = (12, 21, 70)
+    box = seeded_box(dims, 1, seed=8)
+    box[0], box[-1] = 5.0, -3.0
+    box[:, 0], box[:, -1] = 2.0, 7.0
+    box[:, :, 0], box[:, :, -1] = -4.0, 9.0
+    got = sweep(spec, box, 6, arith="fma", k=2)
+    assert np_oracle.max_rel_error(got, oracle(spec, box, 6)) <= FP64_TOL
+
+
+def test_composed3d_fp32():
+    spec = config_spec("c4")
+    box32 = seeded_box((30, 70, 130), 1, seed=12).astype(np.float32)
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 10)
+    got = sweep(spec, box32, 10, arith="fma", k=2)
+    assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+def test_c4_full_size_fma_composed():
+    spec = config_spec("c4")
+    box = seeded_box((512, 512, 512), 1, seed=4)
+    with Plan(spec, (512, 512, 512), k=2, arith="fma") as p:
+        p.upload(box)
+        t = p.run(8)
+        got = p.download()
+    assert t.kernel_name == "compose3d_kernel" and t.launches == 8   # 4 x (main + shell)
+    assert np_oracle.max_rel_error(got, oracle(spec, box, 8)) <= FP64_TOL
+
+
 def test_c4_full_size_exact():
     spec = config_spec("c4")
     box = seeded_box((512, 512, 512), 1, halo="zero")
