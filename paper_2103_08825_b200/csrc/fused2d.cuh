@@ -32,8 +32,14 @@ namespace sb {
 
 constexpr int F2_VX = 4;                 // columns per lane
 constexpr int F2_CW = 32 * F2_VX;        // computed strip width
-constexpr int F2_WARPS = 4;              // warps per CTA
-constexpr int F2_DEPTH = 8;              // staged rows per warp
+#ifndef SB_F2_WARPS
+#define SB_F2_WARPS 4
+#endif
+#ifndef SB_F2_DEPTH
+#define SB_F2_DEPTH 8
+#endif
+constexpr int F2_WARPS = SB_F2_WARPS;    // warps per CTA
+constexpr int F2_DEPTH = SB_F2_DEPTH;    // staged rows per warp
 constexpr int F2_ROWW = F2_CW + 8;       // shared row: 128 columns + edges + pad
 
 struct Item2D {
@@ -170,25 +176,42 @@ fused2d_kernel(const Fused2DParams<T> P) {
         const int ecol = lane == 0 ? xc - 1 : xc + F2_CW;   // strip-edge halo column (lanes 0, 31)
         const bool eload = (lane == 0 || lane == 31) && ecol >= -1 && ecol <= P.nx;
 
-        auto stage = [&](int t) {
-            T* row = ring + (t % RING) * F2_ROWW;
-            const int y = p_first + t;
-            const bool rok = t < M && y >= P.row_lo && y < P.row_hi;
-            const T* g = P.src + P.origin + (int64_t)y * P.sy;
+        // per-item staging state: per-lane source pointers advanced one row per call and
+        // per-lane chunk predicates (rows outside the allocation are warp-uniform)
+        const T* gsrc = P.src + P.origin + (int64_t)p_first * P.sy + xc + F2_VX * lane;
+        const T* gedge = P.src + P.origin + (int64_t)p_first * P.sy + ecol;
+        unsigned chunk_ok = 0;
+#pragma unroll
+        for (int c = 0; c < F2_VX / VEC; c++) {
+            const int x = xc + F2_VX * lane + c * VEC;  // chunk start (16 B aligned)
+            chunk_ok |= (unsigned)(x >= -VEC && x <= P.nx) << c;
+        }
+        int ys = p_first;                               // row of the next stage() call
+        int slot_s = 0;                                 // its ring slot
+        const unsigned soff = static_cast<unsigned>(__cvta_generic_to_shared(ring)) +
+                              (VEC + F2_VX * lane) * (unsigned)sizeof(T);
+        auto stage = [&]() {
+            const bool rok = ys < p_first + M && ys >= P.row_lo && ys < P.row_hi;
+            const unsigned srow = soff + slot_s * (F2_ROWW * (unsigned)sizeof(T));
 #pragma unroll
             for (int c = 0; c < F2_VX / VEC; c++) {
-                const int x = xc + F2_VX * lane + c * VEC;  // chunk start (16 B aligned)
-                const bool ok = rok && x >= -VEC && x <= P.nx;
-                cp_async16(row + VEC + F2_VX * lane + c * VEC, ok ? g + x : P.src, ok);
+                const bool ok = rok && ((chunk_ok >> c) & 1);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(srow + c * 16),
+                             "l"(ok ? gsrc + c * VEC : P.src), "r"(ok ? 16 : 0));
             }
             if (lane == 0 || lane == 31) {
                 const bool ok = rok && eload;
-                cp_async_elem<T>(row + (lane == 0 ? VEC - 1 : VEC + F2_CW), ok ? g + ecol : P.src, ok);
+                cp_async_elem<T>(ring + slot_s * F2_ROWW + (lane == 0 ? VEC - 1 : VEC + F2_CW), ok ? gedge : P.src, ok);
             }
             cp_async_commit();
+            gsrc += P.sy;
+            gedge += P.sy;
+            ys++;
+            slot_s = slot_s + 1 == RING ? 0 : slot_s + 1;
         };
 #pragma unroll
-        for (int t = 0; t < F2_DEPTH - 1; t++) stage(t);
+        for (int t = 0; t < F2_DEPTH - 1; t++) stage();
+        int slot_t = 0;                                 // ring slot of row t
 
         T Pm[K][F2_VX], P0[K][F2_VX];
 #pragma unroll
@@ -199,13 +222,13 @@ fused2d_kernel(const Fused2DParams<T> P) {
         for (int t = 0; t < M; t++) {
             cp_async_wait<F2_DEPTH - 2>();
             __syncwarp();
-            const T* row = ring + (t % RING) * F2_ROWW;
+            const T* row = ring + slot_t * F2_ROWW;
             T v[F2_VX];
 #pragma unroll
             for (int j = 0; j < F2_VX; j++) v[j] = row[VEC + F2_VX * lane + j];
             T edge = lane == 0 ? row[VEC - 1] : row[VEC + F2_CW];
             __syncwarp();                                   // slot t-K-1 fully read before restaging
-            stage(t + F2_DEPTH - 1);
+            stage();                                        // row t + DEPTH - 1
             const int a0 = p_first + t;
             // no level of this row touches a physical y halo and the strip no x halo
             const bool plain = !warp_out && a0 - K >= ylo && a0 - 1 < yhi;
@@ -235,7 +258,8 @@ fused2d_kernel(const Fused2DParams<T> P) {
                     }
                 } else if (warp_out) {                      // x-halo columns of an interior (or ghost) row:
                     // the level-0 value of row yc, still in the ring (zero-filled outside the allocation)
-                    const T* r0 = ring + ((t - l + RING) % RING) * F2_ROWW + VEC + F2_VX * lane;
+                    const int sl = slot_t - l;
+                    const T* r0 = ring + (sl < 0 ? sl + RING : sl) * F2_ROWW + VEC + F2_VX * lane;
 #pragma unroll
                     for (int j = 0; j < F2_VX; j++)
                         if ((out_mask >> j) & 1) done[j] = ((shell_mask >> j) & 1) ? r0[j] : T(0);
@@ -260,6 +284,7 @@ fused2d_kernel(const Fused2DParams<T> P) {
                     }
                 }
             }
+            slot_t = slot_t + 1 == RING ? 0 : slot_t + 1;
         }
         cp_async_wait<0>();
         __syncwarp();
