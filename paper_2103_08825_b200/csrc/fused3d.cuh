@@ -31,6 +31,10 @@
 
 #include "common.cuh"
 
+#ifndef SB_F3_PAIR
+#define SB_F3_PAIR 1    // fp32 box FMA mode: paired accumulators, FFMA2 with broadcast input
+#endif
+
 #ifndef SB_F3_DEBUG
 #define SB_F3_DEBUG 0   // development bisection switches (0 = production)
 #endif
@@ -74,6 +78,7 @@ struct Fused3DParams {
     int total_ctas;
     unsigned int* counter;   // [0] next item, [1] retired CTAs
     T w[27];                 // w[(dz+1)*9 + (dy+1)*3 + (dx+1)]; star uses 7 entries
+    unsigned long long wp[18];   // fp32 box: weight pairs of f3_push_pair
 };
 
 // Output tile geometry.  The TMA box's first column (x0 - K) must be 16 B
@@ -252,6 +257,79 @@ __device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (
         }
 }
 
+// ---- fp32 box, FMA mode: paired accumulators (FFMA2 with a broadcast input).
+// A thread's two x-adjacent points keep each pending sum as one 64-bit register
+// pair (point j=0 low, j=1 high).  An input value x in row column c feeds
+// point j=0 with dx = c-1 and point j=1 with dx = c-2, i.e. the SAME x with two
+// different weights: one FFMA2 (weight pair from the constant bank, x
+// broadcast from a 32-bit register -- no packing moves) updates both points;
+// the edge columns c=0 / c=3 feed one point and take a scalar FFMA on that
+// half.  18 instead of 27 FMA-pipe instructions per point pair and dz group.
+// Each half still receives its terms in canonical (dy, dx) order; the first
+// term is an FMA onto +0 (equal to the rounded product up to the sign of zero).
+__device__ __forceinline__ unsigned long long f2_fma_bcast(unsigned long long w2, float x, unsigned long long acc) {
+    unsigned long long xx, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(w2), "l"(xx), "l"(acc));
+    return d;
+}
+template <int HALF>
+__device__ __forceinline__ unsigned long long f2_fma_half(float w, float x, unsigned long long acc) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
+    if (HALF == 0) lo = __fmaf_rn(w, x, lo);
+    else hi = __fmaf_rn(w, x, hi);
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+
+// wp[(b*3 + dy+1)*2 + c-1] = (w[9b + (dy+1)*3 + c], w[9b + (dy+1)*3 + c-1]) for c in {1, 2}
+__device__ __forceinline__ void f3_push_pair(const float* plane, int tx, int ty, unsigned long long (&Pm)[4],
+                                             unsigned long long (&P0)[4], float (&done)[4][2],
+                                             const float* w, const unsigned long long* wp) {
+    unsigned long long nx[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) nx[i] = 0ull;
+#pragma unroll
+    for (int r = 0; r < 6; r++) {
+        const float* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
+        const float2 a = *reinterpret_cast<const float2*>(row);
+        const float2 b = *reinterpret_cast<const float2*>(row + 2);
+        const float u[4] = {a.x, a.y, b.x, b.y};   // columns 2tx-1 .. 2tx+2
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int dy = r - i - 1;
+            if (dy < -1 || dy > 1) continue;
+            const int q0 = (dy + 1) * 3;          // (dy, dx=-1)
+            // c = 0: point 0, dx = -1
+            Pm[i] = f2_fma_half<0>(w[18 + q0], u[0], Pm[i]);
+            P0[i] = f2_fma_half<0>(w[9 + q0], u[0], P0[i]);
+            nx[i] = f2_fma_half<0>(w[q0], u[0], nx[i]);
+            // c = 1, 2: both points (dx = c-1 for point 0, c-2 for point 1)
+#pragma unroll
+            for (int c = 1; c <= 2; c++) {
+                Pm[i] = f2_fma_bcast(wp[(2 * 3 + dy + 1) * 2 + c - 1], u[c], Pm[i]);
+                P0[i] = f2_fma_bcast(wp[(1 * 3 + dy + 1) * 2 + c - 1], u[c], P0[i]);
+                nx[i] = f2_fma_bcast(wp[(0 * 3 + dy + 1) * 2 + c - 1], u[c], nx[i]);
+            }
+            // c = 3: point 1, dx = +1
+            Pm[i] = f2_fma_half<1>(w[18 + q0 + 2], u[3], Pm[i]);
+            P0[i] = f2_fma_half<1>(w[9 + q0 + 2], u[3], P0[i]);
+            nx[i] = f2_fma_half<1>(w[q0 + 2], u[3], nx[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(done[i][0]), "=f"(done[i][1]) : "l"(Pm[i]));
+        Pm[i] = P0[i];
+        P0[i] = nx[i];
+    }
+}
+
+template <typename T, bool PAIR> struct F3Pend { T v[4][2]; };
+template <typename T> struct F3Pend<T, true> { unsigned long long v[4]; };
+
 template <typename T, bool BOX, int K, bool FMA, int MINB, int NTY>
 __global__ void __launch_bounds__(F3Geo<NTY>::THREADS, MINB)
 fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
@@ -325,13 +403,20 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         if (tid == 0 && SB_F3_DEBUG != 4)
             for (int t = 0; t < F3_NS0 && t < M && (SB_F3_DEBUG != 7 || t < 1); t++) issue(t);
 
-        T Pm[K][4][2], P0[K][4][2];
+        constexpr bool PAIR = sizeof(T) == 4 && FMA && BOX && SB_F3_PAIR;
+        F3Pend<T, PAIR> Pm[K], P0[K];
 #pragma unroll
-        for (int l = 0; l < K; l++)
+        for (int l = 0; l < K; l++) {
+            if constexpr (PAIR) {
 #pragma unroll
-            for (int i = 0; i < 4; i++)
+                for (int i = 0; i < 4; i++) Pm[l].v[i] = P0[l].v[i] = 0ull;
+            } else {
 #pragma unroll
-                for (int j = 0; j < 2; j++) Pm[l][i][j] = P0[l][i][j] = T(0);
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 2; j++) Pm[l].v[i][j] = P0[l].v[i][j] = T(0);
+            }
+        }
 
         for (int t = 0; t < M; t++) {
             const unsigned g = gstep + t;
@@ -342,7 +427,11 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             for (int l = 1; l <= K; l++) {
                 const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE : sl + (l - 2) * PLANE;
                 T done[4][2];
-                f3_push_rows<T, BOX, FMA>(in, tx, ty, Pm[l - 1], P0[l - 1], done, P.w);
+                if constexpr (PAIR)
+                    f3_push_pair(reinterpret_cast<const float*>(in), tx, ty, Pm[l - 1].v, P0[l - 1].v,
+                                 reinterpret_cast<float(&)[4][2]>(done), reinterpret_cast<const float*>(P.w), P.wp);
+                else
+                    f3_push_rows<T, BOX, FMA>(in, tx, ty, Pm[l - 1].v, P0[l - 1].v, done, P.w);
                 const int zc = a0 - l;    // completed level-l plane
                 const bool z_out = (P.phys_lo && zc < 0) || (P.phys_hi && zc >= P.nz);
                 if (z_out) {   // uniform: a physical halo plane, every value is Dirichlet

@@ -1,6 +1,7 @@
 // Launch unit of the fused 3D kernel (K3/K4): TMA descriptors, tile/segment work items.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "plan.hpp"
 #include "fused3d.cuh"
@@ -90,6 +91,17 @@ int launch_fused3d_g(sb_plan* P, int src_idx) {
         const int* o = &P->offsets[3 * i];
         prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
     }
+    auto fbits = [](double v) -> unsigned long long {
+        const float f = (float)v;
+        unsigned int u;
+        memcpy(&u, &f, 4);
+        return u;
+    };
+    for (int b = 0; b < 3; b++)    // weight pairs of f3_push_pair: (point 0 low, point 1 high)
+        for (int dy = 0; dy < 3; dy++)
+            for (int c = 1; c <= 2; c++)
+                prm.wp[(b * 3 + dy) * 2 + c - 1] = (fbits((double)prm.w[9 * b + dy * 3 + c - 1]) << 32) |
+                                                  fbits((double)prm.w[9 * b + dy * 3 + c]);
     P->last_kernel = "fused3d_kernel";
     kern<<<(unsigned)prm.total_ctas, sb::F3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
     SB_CUDA(cudaGetLastError());
@@ -161,7 +173,9 @@ int launch_fused3d_k(sb_plan* P, int src_idx) {
     // 2: 128-thread CTAs, 3 per SM (more registers per thread).  Measured
     // (fp64, T=24): C4 star k=2 499 (geo 2) vs 479 (geo 1); C5 box k=2 374 vs
     // 392; k=3 both 328-390 vs 247-317.  fp32: geo 1 at k <= 2, geo 0 above.
-    const bool geo2 = sizeof(T) == 8 && K >= 2 && !(BOX && K == 2);
+    // fp32 box, paired FFMA2 path (92 registers): 3 CTAs/SM measured best at k <= 2
+    // (C5 fp32 k=2: 626 vs 595 at 4 CTAs/SM; k=1: 568 vs 549)
+    const bool geo2 = (sizeof(T) == 8 && K >= 2 && !(BOX && K == 2)) || (sizeof(T) == 4 && BOX && FMA && K <= 2);
     if (geo == 2 || (geo < 0 && geo2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 3>(P, src_idx);
     if (geo == 1 || (geo < 0 && K <= 2)) return launch_fused3d_g<T, BOX, K, FMA, 4, 4>(P, src_idx);
     return launch_fused3d_g<T, BOX, K, FMA, 8, 2>(P, src_idx);
