@@ -1,13 +1,15 @@
 #!/usr/bin/env python
 """Benchmark of the multistep stencil sweep (BASELINE.json metric).
 
-Workload (N=1): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
+Workload (N=1, default): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
 N=2^26 interior points, T=1000 steps, coefficients (1/16, 1/4, 3/8, 1/4,
 1/16), fixed halo, fused depth k (default: the plan's -- 32 in FMA mode, the
 composed-stencil kernel; ``--sweep-k`` also times k in {1,2,4,8,16,32}).
 One bench "step" = one full sweep (T=1000 time steps over the whole grid).
 At N>1 GPUs the same workload is weak-scaled: each rank owns a 2^26-point
 slab of a 2^26*N-point line, with an r*k-deep ghost exchange every launch.
+``--workload c1|c3a|c3b|c4|c5|c5f32`` runs the other BASELINE configs the same
+way (2D row slabs, 3D z-slabs of the single-GPU size per rank).
 
 Prints ONE JSON line (rank 0).  ``value`` = whole-job GStencil/s with the
 grid resident in HBM (CUDA events on the launching stream, max over ranks);
@@ -40,11 +42,17 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
+# BASELINE.json configs; at N > 1 every workload is weak-scaled along its
+# slowest axis (each rank owns a slab of the single-GPU size).
 WORKLOADS = {
-    "c1": dict(spec="c1", n=1 << 20, T=64, name="1D3P fp64 N=2^20 T=64"),
-    "c2": dict(spec="c2", n=1 << 26, T=1000, name="1D5P fp64 N=2^26 T=1000"),
+    "c1": dict(spec="c1", dims=(1 << 20,), T=64, name="1D3P fp64 N=2^20 T=64"),
+    "c2": dict(spec="c2", dims=(1 << 26,), T=1000, name="1D5P fp64 N=2^26 T=1000"),
+    "c3a": dict(spec="c3a", dims=(16384, 16384), T=500, k=4, name="2D9P fp64 16384^2 T=500 (weights 1/9)"),
+    "c3b": dict(spec="c3b", dims=(16384, 16384), T=500, k=4, name="2D9P fp64 16384^2 T=500 (seeded random weights)"),
+    "c4": dict(spec="c4", dims=(512, 512, 512), T=200, k=2, name="3D7P fp64 512^3 T=200"),
+    "c5": dict(spec="c5", dims=(768, 768, 768), T=100, k=2, name="3D27P fp64 768^3 T=100"),
+    "c5f32": dict(spec="c5", dims=(768, 768, 768), T=100, k=2, dtype="f32", name="3D27P fp32 768^3 T=100"),
 }
-ALG_BYTES_PER_POINT = 16          # fp64 read + write once per fused launch
 
 
 def parse():
@@ -54,7 +62,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
-    ap.add_argument("--k", type=int, default=0, help="fusion depth (0: the plan default, 32 for C2 in FMA mode)")
+    ap.add_argument("--k", type=int, default=0, help="fusion depth (0: the plan default -- 32 for C2 in FMA "
+                                                 "mode, 4 for 2D, 2 for 3D)")
     ap.add_argument("--arith", default="fma", choices=["fma", "exact"])
     ap.add_argument("--sweep-k", action="store_true", help="also time k in {1,2,4,8,16}")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -80,10 +89,11 @@ def measured_peaks():
         with open(fp) as fh:
             f = json.load(fh)
         peaks["fp64_tflops"] = f["fp64_tflops"]
-        peaks["source"]["fp64"] = "measured (profiles/fp_peak.json, tools/fp_peak.cu)"
+        peaks["fp32_tflops"] = f["fp32_tflops"]
+        peaks["source"]["fp64"] = peaks["source"]["fp32"] = "measured (profiles/fp_peak.json, tools/fp_peak.cu)"
     else:
-        peaks["fp64_tflops"] = 37.0
-        peaks["source"]["fp64"] = "datasheet (not measured)"
+        peaks["fp64_tflops"], peaks["fp32_tflops"] = 37.0, 74.0
+        peaks["source"]["fp64"] = peaks["source"]["fp32"] = "datasheet (not measured)"
     return peaks
 
 
@@ -168,14 +178,19 @@ def dist_env():
 
 # ------------------------------------------------------------ CPU reference
 
-def cpu_reference_rate(spec, n, sample_steps=None, budget_s=10.0):
+def seeded_host_box(dims, r, seed=12345):
+    return np.random.default_rng(seed).random(tuple(int(d) + 2 * r for d in dims))
+
+
+def cpu_reference_rate(spec, dims, sample_steps=None, budget_s=10.0):
     """Oracle port (C+OpenMP, all host threads) on a bounded sample of the
     workload grid; returns (GStencil/s, threads, sample description)."""
     from oracle import c_oracle
     from paper_2103_08825_b200.core import canonical
     offs, ws = canonical(spec)
     threads = c_oracle.max_threads()
-    box = np.random.default_rng(12345).random(n + 2 * spec.r)
+    n = int(np.prod(dims))
+    box = seeded_host_box(dims, spec.r)
     t0 = time.perf_counter()
     c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
     one = time.perf_counter() - t0
@@ -185,11 +200,11 @@ def cpu_reference_rate(spec, n, sample_steps=None, budget_s=10.0):
     c_oracle.sweep(box, spec.r, offs, ws, sample_steps, threads=threads, inplace=True)
     dt = time.perf_counter() - t0
     rate = n * sample_steps / dt / 1e9
-    return rate, threads, f"{sample_steps} steps of the full {n}-point grid (same spec)"
+    return rate, threads, f"{sample_steps} steps of the full {'x'.join(map(str, dims))} grid (same spec)"
 
 
 def numpy_reference_rate(spec, n, steps=2):
-    """The reference's own arithmetic as numpy restates it (1 core)."""
+    """The reference's own arithmetic as numpy restates it (1 core; 1D lines)."""
     from oracle import np_oracle
     from paper_2103_08825_b200.core import canonical
     offs, ws = canonical(spec)
@@ -207,12 +222,13 @@ def run_reference_arm(args):
     from paper_2103_08825_b200.core import config_spec
     wl = WORKLOADS[args.workload]
     spec = config_spec(wl["spec"])
-    n = wl["n"]
+    dims = wl["dims"]
+    n = int(np.prod(dims))
     from oracle import c_oracle
     from paper_2103_08825_b200.core import canonical
     offs, ws = canonical(spec)
     threads = c_oracle.max_threads()
-    box = np.random.default_rng(12345).random(n + 2 * spec.r)
+    box = seeded_host_box(dims, spec.r)
     t0 = time.perf_counter()
     c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
     one = time.perf_counter() - t0
@@ -226,12 +242,13 @@ def run_reference_arm(args):
         times.append(time.perf_counter() - t0)
     total = sum(times)
     value = n * per_step * args.steps / total / 1e9
-    sample = f"{per_step} of T={wl['T']} steps of the full {n}-point grid per bench step"
+    sample = (f"{per_step} of T={wl['T']} steps of the full {'x'.join(map(str, dims))} grid per bench step"
+              + (" (fp64 oracle; the reference is fp64-only)" if wl.get("dtype") == "f32" else ""))
     line = {
         "impl": "reference", "metric": "GStencil/s", "value": value, "unit": "GStencil/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": wl.get("dtype", "f64"), "data": "synthetic",
         "config": {"workload": wl["name"], "k": 1, "host": "cpu"},
         "cpu_baseline": {"value": value, "unit": "GStencil/s", "cores": threads,
                          "kind": "port", "sample": sample},
@@ -242,6 +259,19 @@ def run_reference_arm(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+
+def kernel_label(spec, wl, k, arith):
+    """Main kernel a sweep of this workload launches (see sb200.cu / launch*.cu)."""
+    d = len(wl["dims"])
+    if d == 1:
+        return (f"compose1d_kernel<double, {spec.r * k}>" if arith == "fma" and k >= 16
+                else f"fused1d_kernel (K={k})")
+    if d == 2:
+        return f"fused2d_kernel (K={k})"
+    if spec.shape == "star" and arith == "fma" and k == 2 and wl.get("dtype", "f64") == "f64":
+        return "compose3d_kernel (two steps as one 25-point pass)"
+    return f"fused3d_kernel (K={k})"
+
 
 def run_gpu_arm(args):
     import torch
@@ -259,32 +289,33 @@ def run_gpu_arm(args):
     from paper_2103_08825_b200.plan import Plan
     wl = WORKLOADS[args.workload]
     spec = config_spec(wl["spec"])
-    n, T, k = wl["n"], wl["T"], args.k
+    dims, T, k = tuple(wl["dims"]), wl["T"], args.k or wl.get("k", 0)
+    dtype = wl.get("dtype", "f64")
+    torch_dtype = torch.float64 if dtype == "f64" else torch.float32
+    es = 8 if dtype == "f64" else 4
+    n = int(np.prod(dims))                                      # points per GPU
     # a dedicated stream: torch's default (legacy) stream has handle 0, which
     # sb_set_stream treats as "use the plan's own stream"
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-
     rng = np.random.default_rng(12345 + rank)
-    host_in = torch.empty(n + 2 * spec.r, dtype=torch.float64, pin_memory=True)
-    host_in.numpy()[:] = rng.random(n + 2 * spec.r)
-    host_out = torch.empty_like(host_in, pin_memory=True)
 
     if world > 1:
         from paper_2103_08825_b200.slab import SlabSweep
         k = k or (32 if args.arith == "fma" else 16)
-        runner = SlabSweep(spec, (n * world,), rank=rank, world=world, k=k, arith=args.arith,
+        gdims = (dims[0] * world,) + dims[1:]                   # weak scaling along the slowest axis
+        runner = SlabSweep(spec, gdims, rank=rank, world=world, k=k, arith=args.arith, dtype=dtype,
                            device=device, stream_ptr=stream.cuda_stream)
         plan = runner.plan
-        host_in = torch.empty(plan.shape[0], dtype=torch.float64, pin_memory=True)
-        host_in.numpy()[:] = rng.random(plan.shape[0])
-        host_out = torch.empty_like(host_in, pin_memory=True)
         run_once = lambda: runner.run(T)                      # noqa: E731
     else:
-        plan = Plan(spec, (n,), k=k, arith=args.arith, device=device)
+        plan = Plan(spec, dims, k=k, arith=args.arith, dtype=dtype, device=device)
         k = plan.k
         plan.set_stream(stream.cuda_stream)
         run_once = lambda: plan.launch(T)                     # noqa: E731
+    host_in = torch.empty(plan.shape, dtype=torch_dtype, pin_memory=True)
+    host_in.numpy()[...] = rng.random(plan.shape)
+    host_out = torch.empty_like(host_in, pin_memory=True)
     upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
     download = lambda: plan.download(host_out.numpy())       # noqa: E731
 
@@ -325,16 +356,19 @@ def run_gpu_arm(args):
     # duration over the timed region (edge work overlaps it on a side stream).
     launch_ms = ms_per_step / launches_per_step
     peaks = measured_peaks()
+    fp_key = "fp64" if dtype == "f64" else "fp32"
+    fp_peak = peaks[f"{fp_key}_tflops"]
     per_gpu = value / world
     flops_per_update = 2 * len(spec.weights) - 1            # BASELINE's F = 2|W| - 1
-    fp_bound = peaks["fp64_tflops"] * 1e12 / flops_per_update / 1e9
-    hbm_bound = peaks["hbm_gbs"] * 1e9 * k / ALG_BYTES_PER_POINT / 1e9
-    binding = "hbm" if hbm_bound < fp_bound else "fp64"
-    composed = args.arith == "fma" and k >= 16               # compose1d_kernel path (launch1d.cu)
-    kernel_name = f"compose1d_kernel<double, {spec.r * k}>" if composed else f"fused1d_kernel (K={k})"
-    # algorithmic work per launch of k steps: 16 B per point (read + write once),
+    alg_bytes_per_point = 2 * es                              # read + write once per fused launch
+    fp_bound = fp_peak * 1e12 / flops_per_update / 1e9
+    hbm_bound = peaks["hbm_gbs"] * 1e9 * k / alg_bytes_per_point / 1e9
+    binding = "hbm" if hbm_bound < fp_bound else fp_key
+    composed1d = len(dims) == 1 and args.arith == "fma" and k >= 16    # compose1d_kernel (launch1d.cu)
+    kernel_name = kernel_label(spec, wl, k, args.arith)
+    # algorithmic work per launch of k steps: 2s B per point (read + write once),
     # F flops per point update
-    alg_bytes = ALG_BYTES_PER_POINT * n
+    alg_bytes = alg_bytes_per_point * n
     alg_flops = flops_per_update * n * k
     achieved_gbs = alg_bytes / (launch_ms * 1e-3) / 1e9
     achieved_tflops = per_gpu * 1e9 * flops_per_update / 1e12   # = alg_flops / launch time
@@ -343,33 +377,33 @@ def run_gpu_arm(args):
     if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             tj = json.load(fh)
-        if composed and kernel_name in tj["kernel"]:           # the same kernel instantiation
+        if composed1d and kernel_name in tj["kernel"] and args.workload == "c2":   # same kernel and grid
             traffic = tj["traffic_bytes"]
     hbm_view = {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved_gbs / peaks["hbm_gbs"], "alg_bytes_per_launch": alg_bytes,
                 "peak_source": peaks["source"]["hbm"]}
-    fp_view = {"achieved": achieved_tflops, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-               "frac": achieved_tflops / peaks["fp64_tflops"], "alg_flops_per_launch": alg_flops,
-               "peak_source": peaks["source"]["fp64"]}
-    main = fp_view if binding == "fp64" else hbm_view
+    fp_view = {"achieved": achieved_tflops, "peak": fp_peak, "unit": "TFLOP/s",
+               "frac": achieved_tflops / fp_peak, "alg_flops_per_launch": alg_flops,
+               "peak_source": peaks["source"][fp_key]}
+    main = hbm_view if binding == "hbm" else fp_view
     roofline = {
         "bound": binding, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
         "frac": main["frac"], "traffic": traffic,
         "traffic_source": "profiles/r01_bench_kernel_traffic.json (ncu --set full, one launch: "
-                          "dram__bytes_read.sum + dram__bytes_write.sum)",
+                          "dram__bytes_read.sum + dram__bytes_write.sum; C2 only, else null)",
         "kernel": kernel_name, "avg_launch_ms": launch_ms,
-        "note": "bound = the lower of the HBM roofline (16 B/point/launch) and the FP64 roofline "
-                "(F flops/update); 'fp64' is the CUDA-core FP64 pipe (a stencil is not a "
-                "tensor-core contraction)",
-        "hbm": hbm_view, "fp64": fp_view,
+        "note": f"bound = the lower of the HBM roofline ({alg_bytes_per_point} B/point/launch) and the "
+                f"{fp_key.upper()} roofline (F flops/update); '{fp_key}' is the CUDA-core {fp_key.upper()} "
+                "pipe (a stencil is not a tensor-core contraction)",
+        "hbm": hbm_view, fp_key: fp_view,
     }
     stencil_roofline = {
-        "k": k, "hbm_bound_gstencil": hbm_bound, "fp64_bound_gstencil": fp_bound,
+        "k": k, "hbm_bound_gstencil": hbm_bound, f"{fp_key}_bound_gstencil": fp_bound,
         "binding": binding, "achieved_gstencil_per_gpu": per_gpu,
         "frac": per_gpu / min(hbm_bound, fp_bound),
         "note": "frac uses BASELINE's algorithmic F = 2|W|-1 flops per update",
     }
-    if composed:
+    if composed1d:
         # composed-stencil path: (2RK+1) FMAs per point per launch of k steps
         fma_per_update = (2 * spec.r * k + 1) / k
         fma_rate = per_gpu * 1e9 * fma_per_update
@@ -379,13 +413,20 @@ def run_gpu_arm(args):
             "fp64_fma_rate_tflops": 2 * fma_rate / 1e12,
             "fp64_pipe_frac": 2 * fma_rate / (peaks["fp64_tflops"] * 1e12),
         }
+    elif kernel_name.startswith("compose3d"):
+        fma_rate = per_gpu * 1e9 * 12.5                       # 25 FMAs per point per two steps
+        stencil_roofline["executed"] = {
+            "kernel": kernel_name, "fma_per_update": 12.5,
+            "fp64_fma_rate_tflops": 2 * fma_rate / 1e12,
+            "fp64_pipe_frac": 2 * fma_rate / (peaks["fp64_tflops"] * 1e12),
+        }
 
     # End to end through the C-ABI with host buffers: every step uploads its
     # input grid from pinned host memory (H2D), sweeps T steps and downloads
     # the result grid (D2H).  "serial": one plan, the three phases back to
-    # back.  Headline (N=1): independent grids pipelined over two plans on two
-    # streams (sb_upload_async / sb_launch / sb_download_async), so grid i+1's
-    # H2D and grid i-1's D2H run on the copy engines during grid i's sweep.
+    # back.  Headline (N=1): independent grids pipelined over a ring of plans on
+    # their own streams (sb_upload_async / sb_launch / sb_download_async), so
+    # grid i+1's H2D and grid i-1's D2H run on the copy engines during grid i's sweep.
     e2e = None
     if not args.no_e2e:
         barrier()
@@ -402,13 +443,15 @@ def run_gpu_arm(args):
         dt = float(tt.item())
         serial = n * world * T * args.steps / dt / 1e9
         e2e = {"value": serial, "unit": "GStencil/s",
-               "h2d_bytes_per_step": int(host_in.numel() * 8 * world),
-               "d2h_bytes_per_step": int(host_out.numel() * 8 * world),
+               "h2d_bytes_per_step": int(host_in.numel() * es * world),
+               "d2h_bytes_per_step": int(host_out.numel() * es * world),
                "mode": "serial", "timer": "host wall clock around upload+sweep+download, max over ranks"}
+        grid_bytes = host_in.numel() * es
         if world == 1:
             want = host_out.numpy().copy()                       # serial result of the last step
-            NP = 3                                               # plans in the ring
-            plans = [plan] + [Plan(spec, (n,), k=k, arith=args.arith, device=device) for _ in range(NP - 1)]
+            NP = 3 if grid_bytes <= (8 << 30) else 2             # plans in the ring (device memory)
+            plans = [plan] + [Plan(spec, dims, k=k, arith=args.arith, dtype=dtype, device=device)
+                              for _ in range(NP - 1)]
             streams = [stream] + [torch.cuda.Stream() for _ in range(NP - 1)]
             for p, st in zip(plans[1:], streams[1:]):
                 p.set_stream(st.cuda_stream)
@@ -442,45 +485,49 @@ def run_gpu_arm(args):
     sweep = None
     if args.sweep_k and world == 1:
         sweep = {}
-        for kk in (1, 2, 4, 8, 16, 32):
-            with Plan(spec, (n,), k=kk, arith=args.arith, device=device) as p:
+        ks = {1: (1, 2, 4, 8, 16, 32), 2: (1, 2, 4, 8), 3: (1, 2, 3, 4)}[len(dims)]
+        for kk in ks:
+            with Plan(spec, dims, k=kk, arith=args.arith, dtype=dtype, device=device) as p:
                 p.upload(host_in.numpy())
                 p.run(T // 4)
                 tim = p.run(T)
                 g = n * T / (tim.device_ms * 1e-3) / 1e9
-                hb = peaks["hbm_gbs"] * kk / ALG_BYTES_PER_POINT
+                hb = peaks["hbm_gbs"] * kk / alg_bytes_per_point
                 sweep[str(kk)] = {"gstencil": g, "ms": tim.device_ms, "launches": tim.launches,
-                                  "roofline_gstencil": min(hb, fp_bound),
-                                  "binding": "hbm" if hb < fp_bound else "fp64",
+                                  "kernel": tim.kernel_name, "roofline_gstencil": min(hb, fp_bound),
+                                  "binding": "hbm" if hb < fp_bound else fp_key,
                                   "frac": g / min(hb, fp_bound)}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        rate, threads, sample = cpu_reference_rate(spec, n)
+        rate, threads, sample = cpu_reference_rate(spec, dims)
         cpu = {"value": rate, "unit": "GStencil/s", "cores": threads, "kind": "port",
                "sample": sample + "; oracle/oracle.c (bit-exact restatement of "
-                                  "stencilbench scalar_step), OpenMP"}
-        try:
-            cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n)
-        except MemoryError:
-            pass
+                                  "stencilbench scalar_step), OpenMP"
+                                  + (", fp64 (the reference is fp64-only)" if dtype == "f32" else "")}
+        if len(dims) == 1:
+            try:
+                cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n)
+            except MemoryError:
+                pass
 
     if rank == 0:
+        grid_bytes = int(np.prod([d + 2 * spec.r for d in dims])) * es
         line = {
             "metric": "GStencil/s", "value": value, "unit": "GStencil/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
+            "dtype": dtype, "data": "synthetic",
             "config": {"workload": wl["name"] + (f", weak-scaled x{world} (slab per GPU)" if world > 1 else ""),
-                       "k": k, "arith": args.arith, "grid_bytes": (n + 2 * spec.r) * 8,
-                       "l2": "inputs larger than L2 (537 MB grid vs 126 MB L2)"
-                             if n >= (1 << 24) else "grid fits in L2",
+                       "k": k, "arith": args.arith, "grid_bytes": grid_bytes,
+                       "l2": (f"inputs larger than L2 ({grid_bytes / 1e6:.0f} MB grid vs 126 MB L2)"
+                              if grid_bytes > (126 << 20) else "grid fits in L2"),
                        "parallelism": f"slab{world}" if world > 1 else "single"},
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels * world,
-            "gpu_launches_note": "all ranks; per sweep and rank: ceil(T/k) main launches + "
-                                 "the same number of boundary kernels on a side stream",
+            "gpu_launches_note": "all ranks; per sweep and rank: ceil(T/k) main launches + the "
+                                 "boundary / shell kernels on a side stream",
             "clocks": clocks.summary(),
         }
         if sweep is not None:
