@@ -26,4 +26,31 @@ for cfg, dims, ks in (("c2", (5000,), (2, 16)), ("c1", (777,), (8,)), ("c3b", (7
     for s in sw:
         s.upload(s.local_box(gbox))
     run_local(sw, 2 * k + 1)
+# composed 3D star (FMA, k=2: main + shell kernels), incl. z slabs
+spec = config_spec("c4")
+for dims in ((4, 4, 4), (9, 37, 70), (12, 21, 131)):
+    box = rng.random(tuple(n + 2 for n in dims))
+    sweep(spec, box, 5, k=2, arith="fma")
+sw = [SlabSweep(spec, (24, 21, 70), rank=r, world=3, k=2, arith="fma") for r in range(3)]
+gbox = rng.random((26, 23, 72))
+for s in sw:
+    s.upload(s.local_box(gbox))
+run_local(sw, 6)
+# fp32 box, paired FFMA2 path (k=1, 2)
+spec = config_spec("c5")
+box = rng.random((9, 37, 70)).astype(np.float32)
+for k in (1, 2):
+    sweep(spec, box, 2 * k + 1, k=k, arith="fma")
+# layout conversions and storage upload/download
+from paper_2103_08825_b200.grid import Layout, alloc_grid  # noqa: E402
+from paper_2103_08825_b200 import transpose as tr  # noqa: E402
+from paper_2103_08825_b200.kernels import b200_sweep  # noqa: E402
+for cfg, dims, lay, vl in (("c1", (70,), "block_transpose", 4), ("c2", (203,), "dlt", 8),
+                           ("c3b", (9, 45), "block_transpose", 4), ("c4", (5, 6, 50), "dlt", 8)):
+    spec = config_spec(cfg)
+    g = alloc_grid(spec, dims, Layout.NATURAL, vl, pad_for=Layout(lay))
+    g.data[...] = rng.random(g.data.shape)
+    (tr.to_block_transpose if lay == "block_transpose" else tr.to_dlt)(g, vl)
+    b200_sweep(g, spec, 2, 3)
+    (tr.from_block_transpose if lay == "block_transpose" else tr.from_dlt)(g)
 print("sanitize cases done")
