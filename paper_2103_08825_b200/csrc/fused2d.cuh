@@ -63,6 +63,7 @@ struct Fused2DParams {
     unsigned int* counter;   // [0] next item, [1] retired warps
     unsigned long long* trace;   // debug (SB200_TRACE): per item {smid|warp, t0, t1, strip|rows}
     T w[9];                  // w[(dy+1)*3 + (dx+1)]; star uses 5 entries
+    T sa[3], sb[3];          // separable path: w[dy][dx] = sa[dy+1] * sb[dx+1]
 };
 
 // Strip geometry, lane aligned: the K-1 recomputed columns on each side of a
@@ -89,12 +90,26 @@ __device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, bool
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0));
 }
 
-template <typename T, bool BOX, bool FMA>
+template <typename T, bool BOX, bool FMA, bool SEP = false>
 __device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX], T (&P0)[F2_VX], T (&done)[F2_VX],
-                                        const T* w) {
+                                        const T* w, const T* sa = nullptr, const T* sb = nullptr) {
     // u[0] = column -1, u[1..VX] = own columns, u[VX+1] = column VX
     T nx[F2_VX];
-    if (BOX) {
+    if (SEP) {
+        // rank-1 box weights w[dy][dx] = sa[dy] * sb[dx] (FMA mode only): one horizontal
+        // 3-tap pass, then the vertical push -- 6 instead of 9 FMAs per point and level
+        // (same terms, regrouped: within the fp64 bar, not bit-identical)
+        T h[F2_VX];
+#pragma unroll
+        for (int j = 0; j < F2_VX; j++)
+            h[j] = acc_term<T, true>(acc_term<T, true>(acc_first<T, true>(sb[0], u[j]), sb[1], u[j + 1]), sb[2], u[j + 2]);
+#pragma unroll
+        for (int j = 0; j < F2_VX; j++) {
+            Pm[j] = acc_term<T, true>(Pm[j], sa[2], h[j]);      // dy=+1: completes a-1
+            P0[j] = acc_term<T, true>(P0[j], sa[1], h[j]);      // dy= 0
+            nx[j] = acc_first<T, true>(sa[0], h[j]);            // dy=-1
+        }
+    } else if (BOX) {
 #pragma unroll
         for (int q = 0; q < 3; q++) {          // dx = q - 1
 #pragma unroll
@@ -125,7 +140,7 @@ __device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX],
     }
 }
 
-template <typename T, bool BOX, int K, bool FMA>
+template <typename T, bool BOX, int K, bool FMA, bool SEP = false>
 __global__ void __launch_bounds__(F2_WARPS * 32)
 fused2d_kernel(const Fused2DParams<T> P) {
     using TL = F2Tile<T, K>;
@@ -244,7 +259,7 @@ fused2d_kernel(const Fused2DParams<T> P) {
 #pragma unroll
                 for (int j = 0; j < F2_VX; j++) u[j + 1] = v[j];
                 T done[F2_VX];
-                f2_push<T, BOX, FMA>(u, Pm[l - 1], P0[l - 1], done, P.w);
+                f2_push<T, BOX, FMA, SEP>(u, Pm[l - 1], P0[l - 1], done, P.w, P.sa, P.sb);
                 const int yc = a0 - l;                      // completed level-l row
                 const bool y_out = yc < ylo || yc >= yhi;
                 if (!plain && y_out) {                      // (warp-uniform) physical y-halo row

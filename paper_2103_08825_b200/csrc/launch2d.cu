@@ -2,6 +2,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cmath>
+
 #include "plan.hpp"
 #include "fused2d.cuh"
 
@@ -49,10 +51,33 @@ std::vector<sb::Item2D> guided_schedule_2d(int tiles_x, int64_t ny, int64_t warp
     return out;
 }
 
-template <typename T, bool BOX, int K, bool FMA>
+// Rank-1 box weights w[dy][dx] = a[dy] * b[dx] (e.g. C3a's uniform 1/9): the
+// separable push (6 FMAs per point and level instead of 9), FMA mode only.
+bool separable_weights(const sb_plan* P, double a[3], double b[3]) {
+    static const int enabled = (int)env_double("SB200_2D_SEPARABLE", 1);
+    if (!enabled || P->shape != SB_BOX || P->arith != SB_ARITH_FMA || P->nw != 9) return false;
+    double w[3][3] = {};
+    double wmax = 0;
+    for (int i = 0; i < 9; i++) {
+        const int* o = &P->offsets[2 * i];
+        w[o[0] + 1][o[1] + 1] = P->weights[i];
+        wmax = std::max(wmax, std::fabs(P->weights[i]));
+    }
+    if (w[1][1] == 0) return false;
+    for (int i = 0; i < 3; i++) {
+        a[i] = w[i][1];
+        b[i] = w[1][i] / w[1][1];
+    }
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++)
+            if (std::fabs(a[i] * b[j] - w[i][j]) > 1e-14 * wmax) return false;
+    return true;
+}
+
+template <typename T, bool BOX, int K, bool FMA, bool SEP>
 int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     using TL = sb::F2Tile<T, K>;
-    auto kern = sb::fused2d_kernel<T, BOX, K, FMA>;
+    auto kern = sb::fused2d_kernel<T, BOX, K, FMA, SEP>;
     const int smem = sb::fused2d_smem_bytes<T, K>();
     Sched1D* sc = nullptr;
     for (auto& e : P->sched1d)
@@ -99,26 +124,40 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
         const int* o = &P->offsets[2 * i];
         prm.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
     }
+    if (SEP) {
+        double a[3], b[3];
+        separable_weights(P, a, b);
+        for (int i = 0; i < 3; i++) {
+            prm.sa[i] = (T)a[i];
+            prm.sb[i] = (T)b[i];
+        }
+    }
     P->last_kernel = "fused2d_kernel";
     kern<<<(unsigned)blocks, sb::F2_WARPS * 32, smem, P->stream>>>(prm);
     SB_CUDA(cudaGetLastError());
     return SB_OK;
 }
 
-template <typename T, bool BOX, bool FMA>
+template <typename T, bool BOX, bool FMA, bool SEP = false>
 int launch_fused2d_b(sb_plan* P, const T* src, T* dst, int k) {
     switch (k) {
-        case 1: return launch_fused2d_k<T, BOX, 1, FMA>(P, src, dst);
-        case 2: return launch_fused2d_k<T, BOX, 2, FMA>(P, src, dst);
-        case 4: return launch_fused2d_k<T, BOX, 4, FMA>(P, src, dst);
-        case 8: return launch_fused2d_k<T, BOX, 8, FMA>(P, src, dst);
+        case 1: return launch_fused2d_k<T, BOX, 1, FMA, SEP>(P, src, dst);
+        case 2: return launch_fused2d_k<T, BOX, 2, FMA, SEP>(P, src, dst);
+        case 4: return launch_fused2d_k<T, BOX, 4, FMA, SEP>(P, src, dst);
+        case 8: return launch_fused2d_k<T, BOX, 8, FMA, SEP>(P, src, dst);
         default: return fail(SB_ERR_ARG, "unsupported 2D fused depth %d", k);
     }
 }
 
 template <typename T, bool FMA>
 int launch_fused2d_t(sb_plan* P, const T* src, T* dst, int k) {
-    if (P->shape == SB_BOX) return launch_fused2d_b<T, true, FMA>(P, src, dst, k);
+    if (P->shape == SB_BOX) {
+        if constexpr (FMA) {
+            double a[3], b[3];
+            if (separable_weights(P, a, b)) return launch_fused2d_b<T, true, true, true>(P, src, dst, k);
+        }
+        return launch_fused2d_b<T, true, FMA>(P, src, dst, k);
+    }
     return launch_fused2d_b<T, false, FMA>(P, src, dst, k);
 }
 

@@ -279,6 +279,21 @@ def test_c5_full_size_fma():
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
 
 
+# --- separable 2D box (FMA, rank-1 weights: horizontal pass + vertical push)
+
+@pytest.mark.parametrize("k", [1, 2, 4, 8])
+@pytest.mark.parametrize("dims", [(5, 7), (40, 130), (97, 301)])
+def test_separable2d_within_fp64_bar(k, dims):
+    from paper_2103_08825_b200.core import StencilSpec
+    a, b = np.array([0.2, 0.5, 0.3]), np.array([0.15, 0.6, 0.25])
+    w = {(dy, dx): float(a[dy + 1] * b[dx + 1]) for dy in (-1, 0, 1) for dx in (-1, 0, 1)}
+    for spec in (config_spec("c3a"), StencilSpec("rank1", 2, 1, "box", w)):
+        box = seeded_box(dims, 1, seed=sum(dims) + k)
+        T = 2 * k + 3
+        got = sweep(spec, box, T, arith="fma", kernel="fused", k=k)
+        assert np_oracle.max_rel_error(got, oracle(spec, box, T)) <= FP64_TOL
+
+
 # --- composed 3D star (FMA, k=2 as one 25-point pass + exact physical shell)
 
 @pytest.mark.parametrize("dims", [(4, 4, 4), (5, 9, 7), (9, 40, 70), (37, 33, 130), (20, 17, 131)])
