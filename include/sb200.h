@@ -17,6 +17,8 @@
  *   sb_download      <- GridBuffer.natural_interior (core.py:308-316)
  *   sb_step_box      <- scalar_step(..., ranges=...) as driven by the tiled
  *                       runner (tiling.py:353-354)
+ *   sb_launch_range  <- (no reference counterpart: slab edge planes first, then
+ *                       the interior, overlapping the ghost exchange)
  *   sb_upload_storage / sb_download_storage / sb_layout_convert
  *                    <- the layout conversions of transpose.py:266-357
  *                       (BLOCK_TRANSPOSE / DLT storage), see below
@@ -130,6 +132,16 @@ int sb_run(sb_plan *plan, int64_t steps, sb_timing *timing);
 
 /* Same, asynchronously on the plan stream (no host sync, no timing). */
 int sb_launch(sb_plan *plan, int64_t steps);
+
+/* One fused launch of `steps` levels that writes only the slowest-axis
+ * interior positions [lo, hi) of the other buffer, reading the current one.
+ * A step is split into several range launches (e.g. the slab's edge planes
+ * first, then its interior, so the edge planes can be sent to the neighbours
+ * while the interior is computed); the call with finish != 0 completes it
+ * (swaps buffers).  d >= 2; `steps` a fused depth of the plan (1 for generic
+ * plans) and <= the ghost depth / r on slab sides.  Asynchronous on the plan
+ * stream. */
+int sb_launch_range(sb_plan *plan, int64_t steps, int64_t lo, int64_t hi, int32_t finish);
 
 /* One step restricted to the interior sub-box lo[a] <= i_a < hi[a] (first d
  * entries, slowest axis first): the reference's `ranges` argument

@@ -24,7 +24,7 @@ EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_download", "sb_run", "sb_launch", "sb_set_stream", "sb_device_view",
            "sb_plan_k", "sb_kernel_count", "sb_last_error", "sb_abi_version", "sb_device_count",
            "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
-           "sb_upload_storage", "sb_download_storage", "sb_layout_convert")
+           "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range")
 
 
 class SbProblem(ctypes.Structure):
@@ -79,6 +79,7 @@ def load():
     lib.sb_step_box.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
     lib.sb_run.argtypes = [P, ctypes.c_int64, ctypes.POINTER(SbTiming)]
     lib.sb_launch.argtypes = [P, ctypes.c_int64]
+    lib.sb_launch_range.argtypes = [P, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
     lib.sb_set_stream.argtypes = [P, ctypes.c_void_p]
     lib.sb_device_view.argtypes = [P, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.POINTER(ctypes.c_int64), ctypes.c_int64 * 3]
@@ -96,7 +97,7 @@ def load():
     for name in ("sb_plan_create", "sb_host_elems", "sb_upload", "sb_download", "sb_run",
                  "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k", "sb_kernel_count",
                  "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
-                 "sb_upload_storage", "sb_download_storage", "sb_layout_convert"):
+                 "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -60,6 +60,7 @@ struct Compose3DParams {
     int phys_lo, phys_hi;
     int x0_first;            // x origin of the first tile (<= 0; TMA box starts 16 B aligned)
     int tiles_x, tiles_y, nseg, lz, items, total_ctas;
+    int z0, z1;              // output planes [z0, z1) of this launch (range launches)
     unsigned int* counter;
     T w[125];                // composed weights w[c3_widx(dz, dy, dx)], |dz|+|dy|+|dx| <= 2
     T w7[7];                 // the star's own weights, canonical order (x-face correction)
@@ -172,7 +173,7 @@ compose3d_kernel(const __grid_constant__ CUtensorMap tmap, const Compose3DParams
         const bool helper = tx < 8 && (hs == 0 ? face0 : face1);
         const int hqc = (hs == 0 ? -1 : P.nx) - x0 + 2;                  // plane column of q
         T* const obase = P.dst + P.origin + (int64_t)(y0 + 4 * ty) * P.sy + (x0 + 2 * tx);
-        const int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);
+        const int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);
         const int zlo = P.phys_lo ? 1 : 0, zhi = P.phys_hi ? P.nz - 1 : P.nz;   // z shell excluded
         const int p_first = zs0 - 2;
         const int M = (zs1 - zs0) + 4;
@@ -271,6 +272,8 @@ struct Shell3DParams {
     int nx, ny, nz;
     int phys_lo, phys_hi;
     int hz, hz_hi;           // planes allocated below / above the interior
+    int z0, z1;              // output planes [z0, z1) of this launch
+    int zf_lo, zf_hi;        // physical z faces inside [z0, z1) (0 / 1 each)
     int64_t nzf, nyf, nxf;   // points in the z-face, y-face and x-face segments
     T w[7];                  // star weights, canonical order
 };
@@ -278,7 +281,7 @@ struct Shell3DParams {
 template <typename T>
 __global__ void __launch_bounds__(256) compose3d_shell_kernel(const Shell3DParams<T> P) {
     const int64_t total = P.nzf + P.nyf + P.nxf;
-    const int zlo = P.phys_lo ? 1 : 0, zhi = P.phys_hi ? P.nz - 1 : P.nz;
+    const int zlo = max(P.z0, P.phys_lo ? 1 : 0), zhi = min(P.z1, P.phys_hi ? P.nz - 1 : P.nz);
     const int64_t nzi = zhi - zlo > 0 ? zhi - zlo : 0;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(256) compose3d_shell_kernel(const Shell3DParam
             const int64_t per = (int64_t)P.nx * P.ny;
             const int f = (int)(e / per);
             e -= f * per;
-            z = (f == 0 && P.phys_lo) ? 0 : P.nz - 1;
+            z = (f == 0 && P.zf_lo) ? 0 : P.nz - 1;
             y = (int)(e / P.nx);
             x = (int)(e % P.nx);
         } else if ((e -= P.nzf) < P.nyf) {     // y faces, z in [zlo, zhi)

@@ -74,6 +74,7 @@ struct Fused3DParams {
     int phys_lo, phys_hi;    // z sides: physical halo (1) or ghost (0)
     int ghost_lo, ghost_hi;  // ghost depth on slab sides (0 on physical sides)
     int tiles_x, tiles_y, nseg, lz;
+    int z0, z1;              // output planes [z0, z1) of this launch (range launches)
     int items;
     int total_ctas;
     unsigned int* counter;   // [0] next item, [1] retired CTAs
@@ -384,7 +385,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         const int64_t hbase = P.origin + (int64_t)(yc + 4 * ty) * P.sy + (xc + 2 * tx);
         auto hoff = [&](int q) -> int64_t { return hbase + (q >> 1) * P.sy + (q & 1); };
         T* const obase = P.dst + hbase;        // + zc * sz per plane
-        int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);      // output planes
+        int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);   // output planes
         // slab sides: the first/last segment also produces nothing below 0 / above nz
         const int p_first = zs0 - K;
         const int M = (zs1 - zs0) + 2 * K;                      // level-0 arrivals

@@ -71,7 +71,7 @@ fused3d_ws_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<
         const int seg = item / (P.tiles_x * P.tiles_y);
         const int x0 = TL::X0 + tix * TL::TXO, y0 = tiy * TL::TYO;
         const int xc = x0 - (K - 1), yc = y0 - (K - 1);
-        const int zs0 = seg * P.lz, zs1 = min(P.nz, zs0 + P.lz);
+        const int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);
         const int p_first = zs0 - K;
         const int M = (zs1 - zs0) + 2 * K;
 

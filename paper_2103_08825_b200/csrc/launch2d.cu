@@ -80,8 +80,9 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     auto kern = sb::fused2d_kernel<T, BOX, K, FMA, SEP>;
     const int smem = sb::fused2d_smem_bytes<T, K>();
     Sched1D* sc = nullptr;
-    for (auto& e : P->sched1d)
-        if (e.K == 1000 + K) sc = &e;   // 2D schedules keyed by 1000 + K
+    const int64_t y_lo = range_lo(P), y_hi = range_hi(P);
+    for (auto& e : P->sched1d)   // 2D schedules keyed by 1000 + K and the output row range
+        if (e.K == 1000 + K && e.comp_lo == y_lo && e.comp_hi == y_hi) sc = &e;
     if (!sc) {
         SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int occ = 0;
@@ -90,7 +91,13 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
         e.K = 1000 + K;
         e.blocks = P->num_sms * std::max(occ, 1);
         const int tiles_x = (int)((P->dims[1] - TL::X0 + TL::TXO - 1) / TL::TXO);
-        auto items = guided_schedule_2d(tiles_x, P->dims[0], (int64_t)e.blocks * sb::F2_WARPS, K);
+        auto items = guided_schedule_2d(tiles_x, y_hi - y_lo, (int64_t)e.blocks * sb::F2_WARPS, K);
+        for (auto& it : items) {
+            it.ys0 += (int32_t)y_lo;
+            it.ys1 += (int32_t)y_lo;
+        }
+        e.comp_lo = y_lo;
+        e.comp_hi = y_hi;
         e.nchunks = (int)items.size();
         SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Item2D) * items.size()));
         SB_CUDA(cudaMemcpy(e.d_chunks, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice));

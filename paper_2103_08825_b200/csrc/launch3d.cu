@@ -80,9 +80,12 @@ int launch_fused3d_g(sb_plan* P, int src_idx) {
     // small uniform z-segments balance best (measured: k=2 10-16 per CTA, k=1 ~32);
     // each item re-computes a 2K-plane warm-up, so not smaller
     const double seg_env = env_double("SB200_3D_ITEMS_PER_CTA", K == 1 ? 32.0 : 12.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(seg_env * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(seg_env * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((nzr + nseg - 1) / nseg);
+    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
+    prm.z0 = (int)z_lo;
+    prm.z1 = (int)(z_lo + nzr);
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
@@ -144,9 +147,12 @@ int launch_fused3d_ws(sb_plan* P, int src_idx) {
     const int ctas_max = P->num_sms * occ;
     const int tiles = prm.tiles_x * prm.tiles_y;
     const double per = env_double("SB200_3D_ITEMS_PER_CTA", 4.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((nzr + nseg - 1) / nseg);
+    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
+    prm.z0 = (int)z_lo;
+    prm.z1 = (int)(z_lo + nzr);
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
@@ -246,9 +252,12 @@ int launch_compose3d(sb_plan* P, int src_idx) {
     const int ctas_max = P->num_sms * occ;
     const int tiles = prm.tiles_x * prm.tiles_y;
     const double per = env_double("SB200_C3_ITEMS_PER_CTA", 12.0);
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(P->dims[0], (int64_t)(per * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((P->dims[0] + nseg - 1) / nseg);
-    prm.nseg = (int)((P->dims[0] + prm.lz - 1) / prm.lz);
+    const int64_t z_lo = range_lo(P), z_hi = range_hi(P), nzr = z_hi - z_lo;
+    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((nzr + nseg - 1) / nseg);
+    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
+    prm.z0 = (int)z_lo;
+    prm.z1 = (int)z_hi;
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
@@ -270,8 +279,13 @@ int launch_compose3d(sb_plan* P, int src_idx) {
     sp.phys_hi = P->phys_hi;
     sp.hz = (int)P->hlo;
     sp.hz_hi = (int)P->hhi;
-    const int64_t zi = std::max<int64_t>(0, P->dims[0] - (P->phys_lo ? 1 : 0) - (P->phys_hi ? 1 : 0));
-    sp.nzf = (int64_t)(P->phys_lo + P->phys_hi) * prm.nx * prm.ny;
+    sp.z0 = (int)z_lo;
+    sp.z1 = (int)z_hi;
+    sp.zf_lo = P->phys_lo && z_lo == 0;
+    sp.zf_hi = P->phys_hi && z_hi == P->dims[0];
+    const int64_t zi = std::max<int64_t>(0, std::min<int64_t>(z_hi, P->phys_hi ? P->dims[0] - 1 : P->dims[0]) -
+                                                std::max<int64_t>(z_lo, P->phys_lo ? 1 : 0));
+    sp.nzf = (int64_t)(sp.zf_lo + sp.zf_hi) * prm.nx * prm.ny;
     sp.nyf = 2 * zi * prm.nx;
     sp.nxf = 0;   // x faces: corrected inside compose3d_kernel (E(q) push form)
     for (int i = 0; i < 7; i++) sp.w[i] = w7[i];

@@ -98,6 +98,9 @@ struct sb_plan {
     int64_t kernels_launched = 0;   // every kernel launch (sb_kernel_count)
     const char* last_kernel = nullptr;   // main kernel of the last launch (sb_timing.kernel_name)
     int k = 1;
+    // output range on the slowest axis of the next launch ([zr_lo, zr_hi); zr_hi < 0:
+    // the whole interior) -- sb_launch_range, for exchange/compute overlap in slabs
+    int64_t zr_lo = 0, zr_hi = -1;
     int num_sms = 148;
     // host-box geometry
     int64_t host_rows = 0, host_row_elems = 0, host_elems = 0;
@@ -113,6 +116,8 @@ int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
 int make_tensor_maps(sb_plan* P, int geo, int box_h);
 int finish_upload(sb_plan* P);   // buf[0] uploaded: mirror halo/ghost into buf[1], make buf[0] current
+inline int64_t range_lo(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_lo : 0; }
+inline int64_t range_hi(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_hi : P->dims[0]; }
 
 // The composed 1D path (compose1d.cuh) serves depth k when the arithmetic is
 // FMA, R*k <= 64 taps each side, the halo is a whole number of 16 B vectors

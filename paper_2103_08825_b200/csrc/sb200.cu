@@ -161,7 +161,7 @@ int launch_generic(sb_plan* P, const T* src, T* dst, int64_t lo, int64_t hi) {
 
 // One launch advancing k levels from buf[cur] into buf[cur^1].
 template <typename T, bool FMA>
-int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
+int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches, bool swap = true) {
     const T* src = reinterpret_cast<const T*>(P->buf[P->cur]);
     T* dst = reinterpret_cast<T*>(P->buf[P->cur ^ 1]);
     int rc;
@@ -174,12 +174,16 @@ int launch_one(sb_plan* P, int k, int level_in_run, int64_t* launches) {
     } else {
         // generic: one level; on slab sides the valid range shrinks by r per level
         const int64_t n0 = P->dims[0];
-        const int64_t lo = P->phys_lo ? 0 : -P->hlo + (int64_t)P->r * (level_in_run + 1);
-        const int64_t hi = P->phys_hi ? n0 : n0 + P->hhi - (int64_t)P->r * (level_in_run + 1);
+        int64_t lo = P->phys_lo ? 0 : -P->hlo + (int64_t)P->r * (level_in_run + 1);
+        int64_t hi = P->phys_hi ? n0 : n0 + P->hhi - (int64_t)P->r * (level_in_run + 1);
+        if (P->zr_hi >= 0) {   // range launch: interior planes [zr_lo, zr_hi) only
+            lo = P->zr_lo;
+            hi = P->zr_hi;
+        }
         rc = launch_generic<T, FMA>(P, src, dst, lo, hi);
     }
     if (rc != SB_OK) return rc;
-    P->cur ^= 1;
+    if (swap) P->cur ^= 1;
     ++*launches;
     P->kernels_launched++;
     return SB_OK;
@@ -280,6 +284,12 @@ int run_graphed(sb_plan* P, int64_t steps, int64_t* launches, int* k_used) {
     *launches = g->launches;
     *k_used = g->k_used;
     return SB_OK;
+}
+
+template <typename T, bool FMA>
+int launch_range_t(sb_plan* P, int k, bool finish) {
+    int64_t launches = 0;
+    return launch_one<T, FMA>(P, k, 0, &launches, finish);
 }
 
 const char* kernel_name(const sb_plan* P) {
@@ -591,6 +601,37 @@ int sb_launch(sb_plan* P, int64_t steps) {
     int64_t launches = 0;
     int k_used = 1;
     return run_graphed(P, steps, &launches, &k_used);
+}
+
+int sb_launch_range(sb_plan* P, int64_t steps, int64_t lo, int64_t hi, int32_t finish) {
+    if (!P) return fail(SB_ERR_ARG, "NULL plan");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "run before upload");
+    if (P->d < 2) return fail(SB_ERR_ARG, "range launches need d >= 2 (1D slabs exchange r*k points)");
+    const int64_t n0 = P->dims[0];
+    if (lo < 0 || hi > n0 || lo > hi) return fail(SB_ERR_ARG, "range [%lld, %lld) outside [0, %lld)",
+                                                 (long long)lo, (long long)hi, (long long)n0);
+    if (steps > max_slab_steps(P))
+        return fail(SB_ERR_GRID, "slab plan can advance at most %d steps between exchanges", max_slab_steps(P));
+    if (P->kind == KK_GENERIC ? steps != 1 : !fused_k_ok(P, P->kind, (int)steps))
+        return fail(SB_ERR_ARG, "range launch depth %lld unsupported by the plan's kernel", (long long)steps);
+    SB_CUDA(cudaSetDevice(P->device));
+    P->zr_lo = lo;
+    P->zr_hi = hi;
+    int rc = SB_OK;
+    if (hi > lo || finish) {
+        const bool fma = P->arith == SB_ARITH_FMA;
+        if (hi > lo) {
+            if (P->dtype == SB_F64)
+                rc = fma ? launch_range_t<double, true>(P, (int)steps, finish) : launch_range_t<double, false>(P, (int)steps, finish);
+            else
+                rc = fma ? launch_range_t<float, true>(P, (int)steps, finish) : launch_range_t<float, false>(P, (int)steps, finish);
+        } else {
+            P->cur ^= 1;   // empty last part: just complete the step
+        }
+    }
+    P->zr_lo = 0;
+    P->zr_hi = -1;
+    return rc;
 }
 
 int sb_step_box(sb_plan* P, const int64_t* lo, const int64_t* hi) {

@@ -191,6 +191,11 @@ class Plan:
     def launch(self, steps: int) -> None:
         _abi.check(self._lib.sb_launch(self._h, int(steps)))
 
+    def launch_range(self, steps: int, lo: int, hi: int, finish: bool) -> None:
+        """One fused launch writing only slowest-axis interior positions [lo, hi);
+        ``finish`` completes the step (swaps buffers).  Asynchronous."""
+        _abi.check(self._lib.sb_launch_range(self._h, int(steps), int(lo), int(hi), 1 if finish else 0))
+
     def set_stream(self, stream_ptr: int | None) -> None:
         _abi.check(self._lib.sb_set_stream(self._h, ctypes.c_void_p(stream_ptr or 0)))
 

@@ -10,6 +10,10 @@ every fused launch of k steps, ranks exchange G planes with their neighbours
 (grouped isend/irecv), and the fused kernels compute the ghost planes like
 interior ones, so the valid region shrinks back to exactly the slab after k
 steps (overlapped ghost-zone recompute; no exchange inside a launch).
+For 2D/3D slabs the exchange overlaps the compute: each k-step interval first
+computes the G edge planes the neighbours need (``sb_launch_range``), sends
+them from a communication stream while the slab interior is computed on the
+main stream, and the next interval's launches wait for the received ghosts.
 Physical sides keep the Dirichlet halo.  Per-point arithmetic does not
 depend on the decomposition, so results are bit-identical to one GPU.
 
@@ -92,8 +96,21 @@ class DeviceSlab:
         from .plan import Plan
         self.plan = Plan(spec, dims, dtype=dtype, arith=arith, k=k, device=device,
                          ghost=(geom.ghost_lo, geom.ghost_hi))
+        self.stream_ptr = stream_ptr
         if stream_ptr:
             self.plan.set_stream(stream_ptr)
+
+    def torch_stream(self):
+        """The plan's stream as a torch stream (created on first use when the plan
+        runs on its own stream), for event ordering with the exchange."""
+        import torch
+        if getattr(self, "_tstream", None) is None:
+            if self.stream_ptr:
+                self._tstream = torch.cuda.ExternalStream(self.stream_ptr, device=f"cuda:{self.device}")
+            else:
+                self._tstream = torch.cuda.Stream(self.device)
+                self.plan.set_stream(self._tstream.cuda_stream)
+        return self._tstream
         self.geom = geom
         self.itemsize = np.dtype(self.plan.np_dtype).itemsize
         self.typestr = np.dtype(self.plan.np_dtype).str
@@ -108,10 +125,14 @@ class DeviceSlab:
     def launch(self, steps: int):
         self.plan.launch(steps)
 
-    def planes(self, z0: int, count: int):
-        """Tensor view of `count` whole planes starting at local interior plane z0."""
+    def launch_range(self, steps: int, lo: int, hi: int, finish: bool):
+        self.plan.launch_range(steps, lo, hi, finish)
+
+    def planes(self, z0: int, count: int, which: int = 0):
+        """Tensor view of `count` whole planes starting at local interior plane z0
+        of the current (which=0) or the other (which=1) buffer."""
         import torch
-        base, origin, strides = self.plan.device_view(0)
+        base, origin, strides = self.plan.device_view(which)
         pe = strides[0] if self.plan.d > 1 else 1
         first = (origin // pe + z0) * pe if self.plan.d > 1 else origin + z0
         n = count * pe
@@ -152,6 +173,7 @@ class SlabSweep:
 
     def upload(self, local_box: np.ndarray):
         self.backend.upload(local_box)
+        self._fresh = True
 
     def download(self, out=None) -> np.ndarray:
         return self.backend.download(out)
@@ -175,14 +197,78 @@ class SlabSweep:
             req.wait()
         self.exchanges += 1
 
-    def run(self, steps: int):
-        """Advance `steps` time steps: exchange, then one fused launch per k steps."""
+    def run(self, steps: int, overlap: bool | None = None):
+        """Advance `steps` time steps, one fused launch per k steps.
+
+        1D, or ``overlap=False``: exchange, then launch.  2D/3D (default): the
+        exchange of each interval's edge planes overlaps its interior launch
+        (:meth:`_run_overlapped`)."""
+        if overlap is None:
+            overlap = self.spec.d >= 2 and hasattr(self.backend, "launch_range")
+        g = self.geom
+        if overlap and self.world > 1 and g.n >= (g.ghost_lo + g.ghost_hi):
+            return self._run_overlapped(steps)
         done = 0
         ks = _FUSED_KS[self.spec.d]
         while done < steps:
             kk = max(x for x in ks if x <= min(self.k, steps - done))
             self.exchange()
             self.backend.launch(kk)
+            done += kk
+
+    def _run_overlapped(self, steps: int):
+        """Per interval of kk steps: edge planes [0, G) and [n-G, n) first (range
+        launches into the other buffer), their isend/irecv to the neighbours on
+        a communication stream (waiting on an event after the edges), the slab
+        interior [G, n-G) meanwhile on the main stream (completing the step);
+        the next interval's launches wait for the received ghost planes.  The
+        first interval exchanges the uploaded edges up front."""
+        import torch.distributed as dist
+        g = self.geom
+        cuda = isinstance(self.backend, DeviceSlab)
+        if cuda:
+            import torch
+            main = self.backend.torch_stream()
+            comm = getattr(self, "_comm_stream", None) or torch.cuda.Stream(self.backend.device)
+            self._comm_stream = comm
+        e_lo = g.ghost_lo                       # edge planes sent down: [0, G_lo)
+        e_hi = g.n - g.ghost_hi                 # edge planes sent up: [n - G_hi, n)
+        ks = _FUSED_KS[self.spec.d]
+        done = 0
+        if getattr(self, "_fresh", True):
+            self.exchange()                     # ghosts of the uploaded state
+            self._fresh = False
+        while done < steps:
+            kk = max(x for x in ks if x <= min(self.k, steps - done))
+            if e_lo:
+                self.backend.launch_range(kk, 0, e_lo, False)
+            if g.ghost_hi:
+                self.backend.launch_range(kk, e_hi, g.n, False)
+            ops = []
+            if g.ghost_lo:
+                G = g.ghost_lo
+                ops.append(dist.P2POp(dist.isend, self.backend.planes(0, G, 1), self.rank - 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, self.backend.planes(-G, G, 1), self.rank - 1, self.group))
+            if g.ghost_hi:
+                G = g.ghost_hi
+                ops.append(dist.P2POp(dist.isend, self.backend.planes(g.n - G, G, 1), self.rank + 1, self.group))
+                ops.append(dist.P2POp(dist.irecv, self.backend.planes(g.n, G, 1), self.rank + 1, self.group))
+            if cuda:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                with torch.cuda.stream(comm):
+                    comm.wait_event(ev)
+                    reqs = dist.batch_isend_irecv(ops)
+                self.backend.launch_range(kk, e_lo, e_hi, True)     # interior, concurrent with the exchange
+                with torch.cuda.stream(main):                       # main stream waits for the ghosts
+                    for req in reqs:
+                        req.wait()
+                    main.wait_stream(comm)
+            else:
+                for req in dist.batch_isend_irecv(ops):
+                    req.wait()
+                self.backend.launch_range(kk, e_lo, e_hi, True)
+            self.exchanges += 1
             done += kk
 
 
@@ -208,17 +294,46 @@ def exchange_local(sweeps: list[SlabSweep]) -> None:
         torch.cuda.synchronize(d)
 
 
-def run_local(sweeps: list[SlabSweep], steps: int) -> None:
-    """`steps` time steps of a single-process slab set (see exchange_local)."""
+def run_local(sweeps: list[SlabSweep], steps: int, overlap: bool | None = None) -> None:
+    """`steps` time steps of a single-process slab set (see exchange_local).
+
+    2D/3D (default): the same split as SlabSweep._run_overlapped -- edge planes
+    by range launches, their copy into the neighbours' ghost planes of the
+    other buffer, then the slab interiors completing the step."""
     import torch
     ks = _FUSED_KS[sweeps[0].spec.d]
     k = sweeps[0].k
+    if overlap is None:
+        overlap = sweeps[0].spec.d >= 2
     done = 0
+    if overlap:
+        exchange_local(sweeps)
     while done < steps:
         kk = max(x for x in ks if x <= min(k, steps - done))
-        exchange_local(sweeps)
+        if not overlap:
+            exchange_local(sweeps)
+            for s in sweeps:
+                s.backend.launch(kk)
+            done += kk
+            continue
         for s in sweeps:
-            s.backend.launch(kk)
+            g = s.geom
+            if g.ghost_lo:
+                s.backend.launch_range(kk, 0, g.ghost_lo, False)
+            if g.ghost_hi:
+                s.backend.launch_range(kk, g.n - g.ghost_hi, g.n, False)
+        devs = sorted({getattr(s.backend, "device", 0) for s in sweeps})
+        for d in devs:
+            torch.cuda.synchronize(d)
+        for a, b in zip(sweeps[:-1], sweeps[1:]):
+            G = b.geom.ghost_lo
+            b.backend.planes(-G, G, 1).copy_(a.backend.planes(a.geom.n - G, G, 1))
+            a.backend.planes(a.geom.n, G, 1).copy_(b.backend.planes(0, G, 1))
+        for d in devs:
+            torch.cuda.synchronize(d)
+        for s in sweeps:
+            g = s.geom
+            s.backend.launch_range(kk, g.ghost_lo, g.n - g.ghost_hi, True)
         done += kk
     for d in sorted({getattr(s.backend, "device", 0) for s in sweeps}):
         torch.cuda.synchronize(d)

@@ -279,6 +279,31 @@ def test_c5_full_size_fma():
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
 
 
+# --- range launches (slab edge planes first, interior later: sb_launch_range)
+
+@pytest.mark.parametrize("cfg,dims,k,arith", [
+    ("c3b", (60, 130), 4, "exact"), ("c3a", (61, 140), 8, "fma"), ("c4", (30, 37, 70), 2, "fma"),
+    ("c4", (30, 37, 70), 3, "exact"), ("c5", (25, 33, 66), 2, "fma"), ("p:2d5p", (33, 50), 1, "exact"),
+])
+def test_range_launches_compose_a_full_launch(cfg, dims, k, arith):
+    spec = make_stencil_spec(cfg[2:]) if cfg.startswith("p:") else config_spec(cfg)
+    box = seeded_box(dims, spec.r, seed=sum(dims))
+    n0 = dims[0]
+    with Plan(spec, dims, k=k, arith=arith) as p:
+        p.upload(box)
+        p.launch(k)
+        p.synchronize()
+        want = p.download()
+    cuts = [0, 3, n0 - 5, n0]
+    with Plan(spec, dims, k=k, arith=arith) as p:
+        p.upload(box)
+        for i, (lo, hi) in enumerate(zip(cuts[:-1], cuts[1:])):
+            p.launch_range(k, lo, hi, i == len(cuts) - 2)
+        p.synchronize()
+        got = p.download()
+    assert got.tobytes() == want.tobytes()
+
+
 # --- separable 2D box (FMA, rank-1 weights: horizontal pass + vertical push)
 
 @pytest.mark.parametrize("k", [1, 2, 4, 8])

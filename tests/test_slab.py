@@ -55,9 +55,21 @@ class HostSlab:
     def launch(self, steps):
         c_oracle.sweep(self.box, self.spec.r, self.offs, self.ws, steps, threads=1, inplace=True)
 
-    def planes(self, z0, count):
+    def launch_range(self, steps, lo, hi, finish):
+        # the device semantics: parts of one step write [lo, hi) of the other
+        # buffer from the current one; `finish` swaps
+        if getattr(self, "next", None) is None:
+            self.full = c_oracle.sweep(self.box, self.spec.r, self.offs, self.ws, steps, threads=1)
+            self.next = self.box.copy()
+        z = self.geom.h_lo
+        self.next[z + lo:z + hi] = self.full[z + lo:z + hi]
+        if finish:
+            self.box, self.next, self.full = self.next, None, None
+
+    def planes(self, z0, count, which=0):
         z = self.geom.h_lo + z0
-        return torch.from_numpy(self.box[z:z + count]).reshape(-1)
+        arr = self.box if which == 0 else self.next
+        return torch.from_numpy(arr[z:z + count]).reshape(-1)
 
 
 def _free_port():
@@ -66,7 +78,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg, dims, k, steps, outdir):
+def _worker(rank, world, port, cfg, dims, k, steps, outdir, overlap=None):
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     spec = config_spec(cfg) if not cfg.startswith("p:") else make_stencil_spec(cfg[2:])
@@ -74,7 +86,7 @@ def _worker(rank, world, port, cfg, dims, k, steps, outdir):
     geom = slab_geometry(dims[0], spec.r, k, rank, world)
     sw = SlabSweep(spec, dims, rank=rank, world=world, k=k, backend=HostSlab(spec, geom))
     sw.upload(sw.local_box(gbox))
-    sw.run(steps)
+    sw.run(steps, overlap=overlap)
     out = sw.download()
     np.save(os.path.join(outdir, f"r{rank}.npy"), out[geom.interior_slice()])
     np.save(os.path.join(outdir, f"x{rank}.npy"), np.array([sw.exchanges]))
@@ -82,16 +94,17 @@ def _worker(rank, world, port, cfg, dims, k, steps, outdir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cfg,dims,k,steps", [
-    ("c2", (4000,), 8, 37),
-    ("c4", (40, 11, 13), 2, 9),
-    ("c3b", (50, 31), 4, 13),
+@pytest.mark.parametrize("cfg,dims,k,steps,overlap", [
+    ("c2", (4000,), 8, 37, None),
+    ("c4", (40, 11, 13), 2, 9, None),       # 2D/3D default: exchange overlapped with the interior
+    ("c4", (40, 11, 13), 2, 9, False),
+    ("c3b", (50, 31), 4, 13, None),
 ])
-def test_gloo_world2_bit_identical(cfg, dims, k, steps):
+def test_gloo_world2_bit_identical(cfg, dims, k, steps, overlap):
     import torch.multiprocessing as mp
     world = 2
     with tempfile.TemporaryDirectory() as td:
-        mp.spawn(_worker, args=(world, _free_port(), cfg, dims, k, steps, td), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), cfg, dims, k, steps, td, overlap), nprocs=world, join=True)
         got = np.concatenate([np.load(os.path.join(td, f"r{r}.npy")) for r in range(world)], axis=0)
         nex = int(np.load(os.path.join(td, "x0.npy"))[0])
     spec = config_spec(cfg)
