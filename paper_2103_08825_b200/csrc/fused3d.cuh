@@ -35,9 +35,6 @@
 #define SB_F3_PAIR 1    // fp32 box FMA mode: paired accumulators, FFMA2 with broadcast input
 #endif
 
-#ifndef SB_F3_DEBUG
-#define SB_F3_DEBUG 0   // development bisection switches (0 = production)
-#endif
 
 namespace sb {
 
@@ -349,9 +346,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
     if (tid == 0) {
         for (int i = 0; i < F3_NS0; i++) mbar_init(&bar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-#if SB_F3_DEBUG != 1
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
-#endif
     }
     __syncthreads();
 
@@ -394,15 +389,10 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             const unsigned g = gstep + t;
             uint64_t* b = &bar[g % F3_NS0];
             mbar_expect_tx(b, PLANE_BYTES);
-#if SB_F3_DEBUG == 6
-            tma_load_3d(s0 + (g % F3_NS0) * PLANE, &tmap, b, 0, 0, 0);
-#else
-            tma_load_3d(s0 + (g % F3_NS0) * PLANE, &tmap, b, P.ax + x0 - K, P.ry + y0 - K,
-                        P.hz + p_first + t);
-#endif
+            tma_load_3d(s0 + (g % F3_NS0) * PLANE, &tmap, b, P.ax + x0 - K, P.ry + y0 - K, P.hz + p_first + t);
         };
-        if (tid == 0 && SB_F3_DEBUG != 4)
-            for (int t = 0; t < F3_NS0 && t < M && (SB_F3_DEBUG != 7 || t < 1); t++) issue(t);
+        if (tid == 0)
+            for (int t = 0; t < F3_NS0 && t < M; t++) issue(t);
 
         constexpr bool PAIR = sizeof(T) == 4 && FMA && BOX && SB_F3_PAIR;
         F3Pend<T, PAIR> Pm[K], P0[K];
@@ -421,8 +411,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
 
         for (int t = 0; t < M; t++) {
             const unsigned g = gstep + t;
-            if (SB_F3_DEBUG != 4 && !(SB_F3_DEBUG == 5 && t >= F3_NS0) && !(SB_F3_DEBUG == 7 && t >= 1))
-                mbar_wait(&bar[g % F3_NS0], (g / F3_NS0) & 1);
+            mbar_wait(&bar[g % F3_NS0], (g / F3_NS0) & 1);
             const int a0 = p_first + t;   // level-0 plane that arrived
 #pragma unroll
             for (int l = 1; l <= K; l++) {
@@ -470,7 +459,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                     }
                 }
                 if (l < K || K == 1) __syncthreads();
-                if (SB_F3_DEBUG != 4 && SB_F3_DEBUG != 5 && SB_F3_DEBUG != 7 && l == 1 && tid == 0 && t + F3_NS0 < M)
+                if (l == 1 && tid == 0 && t + F3_NS0 < M)
                     issue(t + F3_NS0);   // slot consumed by level 1
             }
             if (K > 1) __syncthreads();   // level K read sl[K-2] before the next step rewrites it

@@ -5,7 +5,6 @@
 
 #include "plan.hpp"
 #include "fused3d.cuh"
-#include "fused3d_ws.cuh"
 #include "compose3d.cuh"
 
 namespace sbh {
@@ -111,70 +110,10 @@ int launch_fused3d_g(sb_plan* P, int src_idx) {
     return SB_OK;
 }
 
-// k = 2 on the warp-specialised level pipeline (fused3d_ws.cuh)
-template <typename T, bool BOX, bool FMA>
-int launch_fused3d_ws(sb_plan* P, int src_idx) {
-    using TL = sb::F3Tile<T, 2, 8>;
-    if (!P->tmap_ok[0]) {
-        const int rc = make_tensor_maps_impl(P, 0, sb::F3Geo<8>::PH);
-        if (rc != SB_OK) return rc;
-    }
-    auto kern = sb::fused3d_ws_kernel<T, BOX, FMA>;
-    const int smem = sb::ws_smem_bytes<T>();
-    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::WS_THREADS, smem));
-    occ = std::max(occ, 1);
-    sb::Fused3DParams<T> prm;
-    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
-    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
-    prm.origin = P->g.origin;
-    prm.sz = P->g.sz;
-    prm.sy = P->g.sy;
-    prm.nz = (int)P->dims[0];
-    prm.ny = (int)P->dims[1];
-    prm.nx = (int)P->dims[2];
-    prm.ax = (int)(P->g.origin % P->g.sy);
-    prm.ry = P->r;
-    prm.hz = (int)P->hlo;
-    prm.hz_hi = (int)P->hhi;
-    prm.phys_lo = P->phys_lo;
-    prm.phys_hi = P->phys_hi;
-    prm.ghost_lo = P->phys_lo ? 0 : (int)P->hlo;
-    prm.ghost_hi = P->phys_hi ? 0 : (int)P->hhi;
-    prm.tiles_x = (int)((P->dims[2] - TL::X0 + TL::TXO - 1) / TL::TXO);
-    prm.tiles_y = (int)((P->dims[1] + TL::TYO - 1) / TL::TYO);
-    const int ctas_max = P->num_sms * occ;
-    const int tiles = prm.tiles_x * prm.tiles_y;
-    const double per = env_double("SB200_3D_ITEMS_PER_CTA", 4.0);
-    const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((nzr + nseg - 1) / nseg);
-    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
-    prm.z0 = (int)z_lo;
-    prm.z1 = (int)(z_lo + nzr);
-    prm.items = tiles * prm.nseg;
-    prm.total_ctas = std::min(ctas_max, prm.items);
-    prm.counter = P->d_counter;
-    for (int i = 0; i < 27; i++) prm.w[i] = T(0);
-    for (int i = 0; i < P->nw; i++) {
-        const int* o = &P->offsets[3 * i];
-        prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
-    }
-    P->last_kernel = "fused3d_ws_kernel";
-    kern<<<(unsigned)prm.total_ctas, sb::WS_THREADS, smem, P->stream>>>(P->tmap[0][src_idx], prm);
-    SB_CUDA(cudaGetLastError());
-    return SB_OK;
-}
-
 template <typename T, bool BOX, int K, bool FMA>
 int launch_fused3d_k(sb_plan* P, int src_idx) {
     // 1: 128-thread CTAs (64 x 16 regions, 4 per SM: barrier phases of different
     // CTAs decorrelate; measured better at K <= 2), 0: 256-thread CTAs (64 x 32)
-    // warp-specialised level pipeline: correct, but measured slower (mbarrier waits + spills at
-    // the 128-register cap: 245 vs 324 GStencil/s on C5 k=2), so opt-in only
-    static const int use_ws = (int)env_double("SB200_3D_WS", 0);
-    if (K == 2 && use_ws) return launch_fused3d_ws<T, BOX, FMA>(P, src_idx);
     static const int geo = (int)env_double("SB200_3D_GEO", -1);
     // 2: 128-thread CTAs, 3 per SM (more registers per thread).  Measured
     // (fp64, T=24): C4 star k=2 499 (geo 2) vs 479 (geo 1); C5 box k=2 374 vs

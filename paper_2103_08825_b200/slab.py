@@ -99,6 +99,10 @@ class DeviceSlab:
         self.stream_ptr = stream_ptr
         if stream_ptr:
             self.plan.set_stream(stream_ptr)
+        self.geom = geom
+        self.itemsize = np.dtype(self.plan.np_dtype).itemsize
+        self.typestr = np.dtype(self.plan.np_dtype).str
+        self.device = device
 
     def torch_stream(self):
         """The plan's stream as a torch stream (created on first use when the plan
@@ -111,10 +115,6 @@ class DeviceSlab:
                 self._tstream = torch.cuda.Stream(self.device)
                 self.plan.set_stream(self._tstream.cuda_stream)
         return self._tstream
-        self.geom = geom
-        self.itemsize = np.dtype(self.plan.np_dtype).itemsize
-        self.typestr = np.dtype(self.plan.np_dtype).str
-        self.device = device
 
     def upload(self, box):
         self.plan.upload(box)
