@@ -44,21 +44,21 @@ constexpr int F3_NS0 = 4;        // TMA ring depth (level-0 planes)
 
 // CTA geometry: NTY thread rows of 32 threads, 2 x 4 points per thread, so the
 // computed region is 64 x (4*NTY) and the plane box 68 x (4*NTY + 2).
-template <int NTY>
+template <int NTY, int RPT = 4>
 struct F3Geo {
     static constexpr int THREADS = 32 * NTY;
-    static constexpr int CH = 4 * NTY;          // computed region height (y)
+    static constexpr int CH = RPT * NTY;        // computed region height (y)
     static constexpr int PH = CH + 2;           // shared plane height: ring + region + ring
 };
 
 // Plane stride in elements: TMA destinations must be 128 B aligned.
-template <typename T, int NTY>
+template <typename T, int NTY, int RPT = 4>
 struct F3Plane {
-    static constexpr int ELEMS = ((F3_PW * F3Geo<NTY>::PH * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
-    static constexpr unsigned BOX_BYTES = F3_PW * F3Geo<NTY>::PH * sizeof(T);
+    static constexpr int ELEMS = ((F3_PW * F3Geo<NTY, RPT>::PH * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
+    static constexpr unsigned BOX_BYTES = F3_PW * F3Geo<NTY, RPT>::PH * sizeof(T);
 };
-template <typename T, int K, int NTY>
-constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T, NTY>::ELEMS * (int)sizeof(T); }
+template <typename T, int K, int NTY, int RPT = 4>
+constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T, NTY, RPT>::ELEMS * (int)sizeof(T); }
 
 template <typename T>
 struct Fused3DParams {
@@ -83,11 +83,11 @@ struct Fused3DParams {
 // aligned (measured: an unaligned innermost coordinate traps with "illegal
 // instruction"), so the tile pitch is a multiple of the 16 B vector and the
 // tiles start at X0 <= 0 with X0 == K (mod VEC); columns x < 0 are not stored.
-template <typename T, int K, int NTY>
+template <typename T, int K, int NTY, int RPT = 4>
 struct F3Tile {
     static constexpr int VEC = 16 / (int)sizeof(T);
     static constexpr int TXO = ((F3_CW - 2 * (K - 1)) / VEC) * VEC;   // output tile width
-    static constexpr int TYO = F3Geo<NTY>::CH - 2 * (K - 1);          // output tile height
+    static constexpr int TYO = F3Geo<NTY, RPT>::CH - 2 * (K - 1);     // output tile height
     static constexpr int X0 = (K % VEC == 0) ? 0 : (K % VEC) - VEC;  // first tile's x origin
 };
 
@@ -119,96 +119,20 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
         : "memory");
 }
 
-// Fold one arriving plane into a level's pending sums (push form along z).
-// v[6][4]: rows 4ty-1..4ty+4, cols 2tx-1..2tx+2 of the computed region.
-// Term-major order: each output still receives its terms in canonical
-// (dy, dx) order within a dz group, but consecutive FMAs in the instruction
-// stream belong to the 8 independent points (ILP 8 instead of one chain).
-template <typename T, bool BOX, bool FMA>
-__device__ __forceinline__ void f3_push(const T (&v)[6][4], T (&Pm)[4][2], T (&P0)[4][2], T (&done)[4][2],
-                                        const T* w) {
-    T nx[4][2];
-    if (BOX) {
-#pragma unroll
-        for (int q = 0; q < 9; q++) {
-            const int dy = q / 3 - 1, dx = q % 3 - 1;
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-#pragma unroll
-                for (int j = 0; j < 2; j++) {
-                    const T x = v[i + 1 + dy][j + 1 + dx];
-                    Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[18 + q], x);      // dz=+1: completes a-1
-                    P0[i][j] = acc_term<T, FMA>(P0[i][j], w[9 + q], x);       // dz= 0: plane a
-                    nx[i][j] = q == 0 ? acc_first<T, FMA>(w[0], x)            // dz=-1: starts a+1
-                                      : acc_term<T, FMA>(nx[i][j], w[q], x);
-                }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) {
-                Pm[i][j] = acc_term<T, FMA>(Pm[i][j], w[22], v[i + 1][j + 1]);   // (1,0,0)
-                P0[i][j] = acc_term<T, FMA>(P0[i][j], w[10], v[i][j + 1]);       // (0,-1,0)
-                nx[i][j] = acc_first<T, FMA>(w[4], v[i + 1][j + 1]);             // (-1,0,0)
-            }
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[12], v[i + 1][j]);      // (0,0,-1)
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[13], v[i + 1][j + 1]);  // (0,0,0)
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[14], v[i + 1][j + 2]);  // (0,0,1)
-#pragma unroll
-        for (int i = 0; i < 4; i++)
-#pragma unroll
-            for (int j = 0; j < 2; j++) P0[i][j] = acc_term<T, FMA>(P0[i][j], w[16], v[i + 2][j + 1]);  // (0,1,0)
-    }
-#pragma unroll
-    for (int i = 0; i < 4; i++)
-#pragma unroll
-        for (int j = 0; j < 2; j++) {
-            done[i][j] = Pm[i][j];
-            Pm[i][j] = P0[i][j];
-            P0[i][j] = nx[i][j];
-        }
-}
-
-template <typename T>
-__device__ __forceinline__ void f3_read(const T* plane, int tx, int ty, T (&v)[6][4]) {
-#pragma unroll
-    for (int r = 0; r < 6; r++) {
-        const T* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
-        if (sizeof(T) == 8) {
-            const double2 a = *reinterpret_cast<const double2*>(row);
-            const double2 b = *reinterpret_cast<const double2*>(row + 2);
-            v[r][0] = (T)a.x; v[r][1] = (T)a.y; v[r][2] = (T)b.x; v[r][3] = (T)b.y;
-        } else {
-            const float2 a = *reinterpret_cast<const float2*>(row);
-            const float2 b = *reinterpret_cast<const float2*>(row + 2);
-            v[r][0] = (T)a.x; v[r][1] = (T)a.y; v[r][2] = (T)b.x; v[r][3] = (T)b.y;
-        }
-    }
-}
-
-// Row-streaming form of f3_read + f3_push: the arriving plane is read one row
-// (4 values) at a time and folded into the point-rows it touches, so only 4
-// plane values are live instead of 24.  Rows arrive in increasing dy and dx
+// Fold one arriving plane into a level's pending sums (push form along z),
+// streaming the plane one row (4 values) at a time into the point-rows it
+// touches, so only 4 plane values are live.  Term-major order: consecutive
+// FMAs in the instruction stream belong to independent points (ILP 2*RPT).  Rows arrive in increasing dy and dx
 // ascends within a row, so each accumulator still receives its terms in
 // canonical (dy, dx) order within its dz group.
-template <typename T, bool BOX, bool FMA>
-__device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (&Pm)[4][2], T (&P0)[4][2],
-                                             T (&done)[4][2], const T* w) {
-    T nx[4][2];
+template <typename T, bool BOX, bool FMA, int RPT = 4>
+__device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (&Pm)[RPT][2], T (&P0)[RPT][2],
+                                             T (&done)[RPT][2], const T* w) {
+    T nx[RPT][2];
 #pragma unroll
-    for (int r = 0; r < 6; r++) {
+    for (int r = 0; r < RPT + 2; r++) {
         T u[4];
-        const T* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
+        const T* row = plane + (RPT * ty + r) * F3_PW + 2 * tx;
         if (sizeof(T) == 8) {
             const double2 a = *reinterpret_cast<const double2*>(row);
             const double2 b = *reinterpret_cast<const double2*>(row + 2);
@@ -219,7 +143,7 @@ __device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (
             u[0] = (T)a.x; u[1] = (T)a.y; u[2] = (T)b.x; u[3] = (T)b.y;
         }
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
+        for (int i = 0; i < RPT; i++) {
             const int dy = r - i - 1;                   // this row's dy for point-row i
             if (dy < -1 || dy > 1) continue;
 #pragma unroll
@@ -246,7 +170,7 @@ __device__ __forceinline__ void f3_push_rows(const T* plane, int tx, int ty, T (
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++)
+    for (int i = 0; i < RPT; i++)
 #pragma unroll
         for (int j = 0; j < 2; j++) {
             done[i][j] = Pm[i][j];
@@ -283,20 +207,21 @@ __device__ __forceinline__ unsigned long long f2_fma_half(float w, float x, unsi
 }
 
 // wp[(b*3 + dy+1)*2 + c-1] = (w[9b + (dy+1)*3 + c], w[9b + (dy+1)*3 + c-1]) for c in {1, 2}
-__device__ __forceinline__ void f3_push_pair(const float* plane, int tx, int ty, unsigned long long (&Pm)[4],
-                                             unsigned long long (&P0)[4], float (&done)[4][2],
+template <int RPT = 4>
+__device__ __forceinline__ void f3_push_pair(const float* plane, int tx, int ty, unsigned long long (&Pm)[RPT],
+                                             unsigned long long (&P0)[RPT], float (&done)[RPT][2],
                                              const float* w, const unsigned long long* wp) {
-    unsigned long long nx[4];
+    unsigned long long nx[RPT];
 #pragma unroll
-    for (int i = 0; i < 4; i++) nx[i] = 0ull;
+    for (int i = 0; i < RPT; i++) nx[i] = 0ull;
 #pragma unroll
-    for (int r = 0; r < 6; r++) {
-        const float* row = plane + (4 * ty + r) * F3_PW + 2 * tx;
+    for (int r = 0; r < RPT + 2; r++) {
+        const float* row = plane + (RPT * ty + r) * F3_PW + 2 * tx;
         const float2 a = *reinterpret_cast<const float2*>(row);
         const float2 b = *reinterpret_cast<const float2*>(row + 2);
         const float u[4] = {a.x, a.y, b.x, b.y};   // columns 2tx-1 .. 2tx+2
 #pragma unroll
-        for (int i = 0; i < 4; i++) {
+        for (int i = 0; i < RPT; i++) {
             const int dy = r - i - 1;
             if (dy < -1 || dy > 1) continue;
             const int q0 = (dy + 1) * 3;          // (dy, dx=-1)
@@ -318,23 +243,24 @@ __device__ __forceinline__ void f3_push_pair(const float* plane, int tx, int ty,
         }
     }
 #pragma unroll
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < RPT; i++) {
         asm("mov.b64 {%0, %1}, %2;" : "=f"(done[i][0]), "=f"(done[i][1]) : "l"(Pm[i]));
         Pm[i] = P0[i];
         P0[i] = nx[i];
     }
 }
 
-template <typename T, bool PAIR> struct F3Pend { T v[4][2]; };
-template <typename T> struct F3Pend<T, true> { unsigned long long v[4]; };
+template <typename T, bool PAIR, int RPT> struct F3Pend { T v[RPT][2]; };
+template <typename T, int RPT> struct F3Pend<T, true, RPT> { unsigned long long v[RPT]; };
 
-template <typename T, bool BOX, int K, bool FMA, int MINB, int NTY>
-__global__ void __launch_bounds__(F3Geo<NTY>::THREADS, MINB)
+// RPT: point rows per thread (each thread owns 2 x RPT points of the region)
+template <typename T, bool BOX, int K, bool FMA, int MINB, int NTY, int RPT = 4>
+__global__ void __launch_bounds__(F3Geo<NTY, RPT>::THREADS, MINB)
 fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> P) {
-    constexpr int PLANE = F3Plane<T, NTY>::ELEMS;
-    constexpr unsigned PLANE_BYTES = F3Plane<T, NTY>::BOX_BYTES;
-    constexpr int F3_CH = F3Geo<NTY>::CH;
-    using TL = F3Tile<T, K, NTY>;
+    constexpr int PLANE = F3Plane<T, NTY, RPT>::ELEMS;
+    constexpr unsigned PLANE_BYTES = F3Plane<T, NTY, RPT>::BOX_BYTES;
+    constexpr int NPT = 2 * RPT;                  // points per thread
+    using TL = F3Tile<T, K, NTY, RPT>;
     extern __shared__ __align__(1024) unsigned char smem3d[];   // TMA destinations: 128 B aligned
     T* s0 = reinterpret_cast<T*>(smem3d);              // NS0 level-0 slots
     T* sl = s0 + F3_NS0 * PLANE;                       // levels 1..K-1, one plane each
@@ -366,8 +292,8 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
         // and the points this thread stores at level K (inside the output tile and the grid)
         unsigned out_mask = 0, shell_mask = 0, store_mask = 0;
 #pragma unroll
-        for (int q = 0; q < 8; q++) {
-            const int y = yc + 4 * ty + (q >> 1), x = xc + 2 * tx + (q & 1);
+        for (int q = 0; q < NPT; q++) {
+            const int y = yc + RPT * ty + (q >> 1), x = xc + 2 * tx + (q & 1);
             const bool out = x < 0 || x >= P.nx || y < 0 || y >= P.ny;
             const bool shell = x >= -1 && x <= P.nx && y >= -1 && y <= P.ny;
             const int ri = y - y0, cj = x - x0;
@@ -377,7 +303,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             store_mask |= (unsigned)st << q;
         }
         // in-plane element offset of point (0, 0); point q is + (q >> 1) * sy + (q & 1)
-        const int64_t hbase = P.origin + (int64_t)(yc + 4 * ty) * P.sy + (xc + 2 * tx);
+        const int64_t hbase = P.origin + (int64_t)(yc + RPT * ty) * P.sy + (xc + 2 * tx);
         auto hoff = [&](int q) -> int64_t { return hbase + (q >> 1) * P.sy + (q & 1); };
         T* const obase = P.dst + hbase;        // + zc * sz per plane
         int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);   // output planes
@@ -395,15 +321,15 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             for (int t = 0; t < F3_NS0 && t < M; t++) issue(t);
 
         constexpr bool PAIR = sizeof(T) == 4 && FMA && BOX && SB_F3_PAIR;
-        F3Pend<T, PAIR> Pm[K], P0[K];
+        F3Pend<T, PAIR, RPT> Pm[K], P0[K];
 #pragma unroll
         for (int l = 0; l < K; l++) {
             if constexpr (PAIR) {
 #pragma unroll
-                for (int i = 0; i < 4; i++) Pm[l].v[i] = P0[l].v[i] = 0ull;
+                for (int i = 0; i < RPT; i++) Pm[l].v[i] = P0[l].v[i] = 0ull;
             } else {
 #pragma unroll
-                for (int i = 0; i < 4; i++)
+                for (int i = 0; i < RPT; i++)
 #pragma unroll
                     for (int j = 0; j < 2; j++) Pm[l].v[i][j] = P0[l].v[i][j] = T(0);
             }
@@ -416,18 +342,18 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
 #pragma unroll
             for (int l = 1; l <= K; l++) {
                 const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE : sl + (l - 2) * PLANE;
-                T done[4][2];
+                T done[RPT][2];
                 if constexpr (PAIR)
-                    f3_push_pair(reinterpret_cast<const float*>(in), tx, ty, Pm[l - 1].v, P0[l - 1].v,
-                                 reinterpret_cast<float(&)[4][2]>(done), reinterpret_cast<const float*>(P.w), P.wp);
+                    f3_push_pair<RPT>(reinterpret_cast<const float*>(in), tx, ty, Pm[l - 1].v, P0[l - 1].v,
+                                 reinterpret_cast<float(&)[RPT][2]>(done), reinterpret_cast<const float*>(P.w), P.wp);
                 else
-                    f3_push_rows<T, BOX, FMA>(in, tx, ty, Pm[l - 1].v, P0[l - 1].v, done, P.w);
+                    f3_push_rows<T, BOX, FMA, RPT>(in, tx, ty, Pm[l - 1].v, P0[l - 1].v, done, P.w);
                 const int zc = a0 - l;    // completed level-l plane
                 const bool z_out = (P.phys_lo && zc < 0) || (P.phys_hi && zc >= P.nz);
                 if (z_out) {   // uniform: a physical halo plane, every value is Dirichlet
                     const bool z_shell = zc >= -1 && zc <= P.nz;
 #pragma unroll
-                    for (int q = 0; q < 8; q++) {
+                    for (int q = 0; q < NPT; q++) {
                         T hv = T(0);
                         if (z_shell && ((shell_mask >> q) & 1)) hv = P.src[hoff(q) + (int64_t)zc * P.sz];
                         done[q >> 1][q & 1] = hv;
@@ -437,7 +363,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                     // segment) are garbage that never reaches a valid output: no load
                     const bool z_alloc = zc >= -P.hz && zc < P.nz + P.hz_hi;
 #pragma unroll
-                    for (int q = 0; q < 8; q++)
+                    for (int q = 0; q < NPT; q++)
                         if ((out_mask >> q) & 1)
                             done[q >> 1][q & 1] =
                                 (z_alloc && ((shell_mask >> q) & 1)) ? P.src[hoff(q) + (int64_t)zc * P.sz] : T(0);
@@ -445,13 +371,13 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                 if (l < K) {
                     T* o = sl + (l - 1) * PLANE;
 #pragma unroll
-                    for (int i = 0; i < 4; i++)
+                    for (int i = 0; i < RPT; i++)
 #pragma unroll
-                        for (int j = 0; j < 2; j++) o[(4 * ty + i + 1) * F3_PW + 2 * tx + j + 1] = done[i][j];
+                        for (int j = 0; j < 2; j++) o[(RPT * ty + i + 1) * F3_PW + 2 * tx + j + 1] = done[i][j];
                 } else if (zc >= zs0 && zc < zs1 && store_mask) {
                     T* row = obase + (int64_t)zc * P.sz;
 #pragma unroll
-                    for (int i = 0; i < 4; i++) {
+                    for (int i = 0; i < RPT; i++) {
 #pragma unroll
                         for (int j = 0; j < 2; j++)
                             if ((store_mask >> (2 * i + j)) & 1) row[j] = done[i][j];

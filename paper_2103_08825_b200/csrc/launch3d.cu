@@ -41,19 +41,21 @@ int make_tensor_maps_impl(sb_plan* P, int geo, int box_h) {
     return SB_OK;
 }
 
-template <typename T, bool BOX, int K, bool FMA, int NTY, int MINB>
+template <typename T, bool BOX, int K, bool FMA, int NTY, int MINB, int RPT = 4>
 int launch_fused3d_g(sb_plan* P, int src_idx) {
-    using TL = sb::F3Tile<T, K, NTY>;
-    constexpr int GEO = NTY == 8 ? 0 : 1;
+    using TL = sb::F3Tile<T, K, NTY, RPT>;
+    using GEOM = sb::F3Geo<NTY, RPT>;
+    static_assert(GEOM::PH == 34 || GEOM::PH == 18, "tensor-map slots exist for plane heights 34 and 18");
+    constexpr int GEO = GEOM::PH == 34 ? 0 : 1;   // TMA box height (slot shared by equal heights)
     if (!P->tmap_ok[GEO]) {
-        const int rc = make_tensor_maps_impl(P, GEO, sb::F3Geo<NTY>::PH);
+        const int rc = make_tensor_maps_impl(P, GEO, GEOM::PH);
         if (rc != SB_OK) return rc;
     }
-    auto kern = sb::fused3d_kernel<T, BOX, K, FMA, MINB, NTY>;
-    const int smem = sb::f3_smem_bytes<T, K, NTY>();
+    auto kern = sb::fused3d_kernel<T, BOX, K, FMA, MINB, NTY, RPT>;
+    const int smem = sb::f3_smem_bytes<T, K, NTY, RPT>();
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int occ = 0;
-    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, sb::F3Geo<NTY>::THREADS, smem));
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GEOM::THREADS, smem));
     occ = std::max(occ, 1);
     sb::Fused3DParams<T> prm;
     prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
@@ -105,7 +107,7 @@ int launch_fused3d_g(sb_plan* P, int src_idx) {
                 prm.wp[(b * 3 + dy) * 2 + c - 1] = (fbits((double)prm.w[9 * b + dy * 3 + c - 1]) << 32) |
                                                   fbits((double)prm.w[9 * b + dy * 3 + c]);
     P->last_kernel = "fused3d_kernel";
-    kern<<<(unsigned)prm.total_ctas, sb::F3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
+    kern<<<(unsigned)prm.total_ctas, GEOM::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
     SB_CUDA(cudaGetLastError());
     return SB_OK;
 }
