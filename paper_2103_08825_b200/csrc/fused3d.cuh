@@ -40,7 +40,14 @@ namespace sb {
 
 constexpr int F3_CW = 64;        // computed region width (x)
 constexpr int F3_PW = 68;        // shared plane width: ring + region + pad (16 B rows)
-constexpr int F3_NS0 = 4;        // TMA ring depth (level-0 planes)
+#ifndef SB_F3_NS0
+#define SB_F3_NS0 4
+#endif
+#ifndef SB_F3_DBL
+#define SB_F3_DBL 0     // double-buffered level planes: no end-of-plane barrier
+#endif
+constexpr int F3_NS0 = SB_F3_NS0;   // TMA ring depth (level-0 planes)
+constexpr int F3_NB = SB_F3_DBL ? 2 : 1;   // buffers per level plane
 
 // CTA geometry: NTY thread rows of 32 threads, 2 x 4 points per thread, so the
 // computed region is 64 x (4*NTY) and the plane box 68 x (4*NTY + 2).
@@ -58,7 +65,7 @@ struct F3Plane {
     static constexpr unsigned BOX_BYTES = F3_PW * F3Geo<NTY, RPT>::PH * sizeof(T);
 };
 template <typename T, int K, int NTY, int RPT = 4>
-constexpr int f3_smem_bytes() { return (F3_NS0 + K - 1) * F3Plane<T, NTY, RPT>::ELEMS * (int)sizeof(T); }
+constexpr int f3_smem_bytes() { return (F3_NS0 + F3_NB * (K - 1)) * F3Plane<T, NTY, RPT>::ELEMS * (int)sizeof(T); }
 
 template <typename T>
 struct Fused3DParams {
@@ -341,7 +348,8 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
             const int a0 = p_first + t;   // level-0 plane that arrived
 #pragma unroll
             for (int l = 1; l <= K; l++) {
-                const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE : sl + (l - 2) * PLANE;
+                const T* in = (l == 1) ? s0 + (g % F3_NS0) * PLANE
+                                       : sl + ((l - 2) * F3_NB + (SB_F3_DBL ? (t & 1) : 0)) * PLANE;
                 T done[RPT][2];
                 if constexpr (PAIR)
                     f3_push_pair<RPT>(reinterpret_cast<const float*>(in), tx, ty, Pm[l - 1].v, P0[l - 1].v,
@@ -369,7 +377,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                                 (z_alloc && ((shell_mask >> q) & 1)) ? P.src[hoff(q) + (int64_t)zc * P.sz] : T(0);
                 }
                 if (l < K) {
-                    T* o = sl + (l - 1) * PLANE;
+                    T* o = sl + ((l - 1) * F3_NB + (SB_F3_DBL ? (t & 1) : 0)) * PLANE;
 #pragma unroll
                     for (int i = 0; i < RPT; i++)
 #pragma unroll
@@ -388,7 +396,7 @@ fused3d_kernel(const __grid_constant__ CUtensorMap tmap, const Fused3DParams<T> 
                 if (l == 1 && tid == 0 && t + F3_NS0 < M)
                     issue(t + F3_NS0);   // slot consumed by level 1
             }
-            if (K > 1) __syncthreads();   // level K read sl[K-2] before the next step rewrites it
+            if (K > 1 && !SB_F3_DBL) __syncthreads();   // level K read sl[K-2] before the next step rewrites it
         }
         gstep += M;
     }
