@@ -63,7 +63,7 @@ struct Compose3DParams {
     int z0, z1;              // output planes [z0, z1) of this launch (range launches)
     unsigned int* counter;
     T w[125];                // composed weights w[c3_widx(dz, dy, dx)], |dz|+|dy|+|dx| <= 2
-    T w7[7];                 // the star's own weights, canonical order (x-face correction)
+    T wx[2][125];            // exact two-step weights of the x = 0 / x = nx-1 face points
 };
 
 // Fold one arriving plane a into the four pending outputs A[0] = a-2 (its
@@ -168,10 +168,11 @@ compose3d_kernel(const __grid_constant__ CUtensorMap tmap, const Compose3DParams
         const bool face0 = x0 <= 0, face1 = x0 + C3_CW > P.nx - 1;
         const int own0 = (0 - x0) >> 1, own1 = (P.nx - 1 - x0) >> 1;    // owner lanes
         const int oj0 = (0 - x0) & 1, oj1 = (P.nx - 1 - x0) & 1;         // owner point column
-        // helper lanes 0-3 (side 0) and 4-7 (side 1) each carry E for one row of the warp
+        // helper lanes 0-3 (side 0) and 4-7 (side 1) each evaluate one row's x-face point
         const int hs = tx >> 2, hrow = tx & 3;
         const bool helper = tx < 8 && (hs == 0 ? face0 : face1);
-        const int hqc = (hs == 0 ? -1 : P.nx) - x0 + 2;                  // plane column of q
+        const int hpc = (hs == 0 ? 0 : P.nx - 1) - x0 + 2;                // plane column of the point
+        const T* const wf = P.wx[hs];
         T* const obase = P.dst + P.origin + (int64_t)(y0 + 4 * ty) * P.sy + (x0 + 2 * tx);
         const int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);
         const int zlo = P.phys_lo ? 1 : 0, zhi = P.phys_hi ? P.nz - 1 : P.nz;   // z shell excluded
@@ -187,9 +188,9 @@ compose3d_kernel(const __grid_constant__ CUtensorMap tmap, const Compose3DParams
         if (tid == 0)
             for (int t = 0; t < C3_NS && t < M; t++) issue(t);
 
-        // E(q) = S~(u)(q) - u(q) at the halo neighbour q of an x-face point, in push form
-        // along z: Eh = complete (plane a-2), E1 = plane a-1, E0 = plane a (helper lanes)
-        T Eh = T(0), E1 = T(0), E0 = T(0);
+        // helper lanes: the x-face point's own 25-tap push (weights wx[side]), pending
+        // outputs a-2 .. a+1 as in c3_push
+        T H0 = T(0), H1 = T(0), H2 = T(0), H3 = T(0);
         T A[4][4][2];
 #pragma unroll
         for (int s = 0; s < 4; s++)
@@ -205,32 +206,45 @@ compose3d_kernel(const __grid_constant__ CUtensorMap tmap, const Compose3DParams
             const T* pl = s0 + (g % C3_NS) * PLANE;
             c3_push<T>(pl, tx, ty, A, done, P.w);
             if (face0 || face1) {
-                // exact(p) = composed(p) - w_face * E(q): the composition used the stencil value
-                // at the halo point q where the true intermediate value is the halo u(q)
+                // x-face points are not compositions (one neighbour is the held halo): their
+                // exact two-step value is a 25-tap sum too, with the folded weights wx[side]
+                // (no subtraction, so NaN / Inf propagate as in the level-by-level sweep)
+                T hd = T(0);
+                if (helper) {
+                    const T* pp = pl + (4 * ty + hrow + 2) * C3_PW + hpc;   // the point in plane a
+                    T nxt = T(0);
+#pragma unroll
+                    for (int dy = -2; dy <= 2; dy++)
+#pragma unroll
+                        for (int dx = -2; dx <= 2; dx++) {
+                            const int m = (dy < 0 ? -dy : dy) + (dx < 0 ? -dx : dx);
+                            if (m > 2) continue;
+                            const T v = pp[dy * C3_PW + dx];
+                            if (m == 0) {
+                                H0 = acc_term<T, true>(H0, wf[c3_widx(2, 0, 0)], v);
+                                nxt = acc_first<T, true>(wf[c3_widx(-2, 0, 0)], v);
+                            }
+                            if (m <= 1) H1 = acc_term<T, true>(H1, wf[c3_widx(1, dy, dx)], v);
+                            H2 = acc_term<T, true>(H2, wf[c3_widx(0, dy, dx)], v);
+                            if (m <= 1) H3 = acc_term<T, true>(H3, wf[c3_widx(-1, dy, dx)], v);
+                        }
+                    hd = H0;
+                    H0 = H1;
+                    H1 = H2;
+                    H2 = H3;
+                    H3 = nxt;
+                }
 #pragma unroll
                 for (int sd = 0; sd < 2; sd++) {
                     if (!(sd == 0 ? face0 : face1)) continue;
-                    const T wf = sd == 0 ? P.w7[2] : P.w7[4];
                     const int own = sd == 0 ? own0 : own1, oj = sd == 0 ? oj0 : oj1;
 #pragma unroll
                     for (int i = 0; i < 4; i++) {
-                        const T e = __shfl_sync(0xffffffffu, Eh, sd * 4 + i);
+                        const T e = __shfl_sync(0xffffffffu, hd, sd * 4 + i);
 #pragma unroll
                         for (int j = 0; j < 2; j++)
-                            if (tx == own && j == oj) done[i][j] = acc_term<T, true>(done[i][j], -wf, e);
+                            if (tx == own && j == oj) done[i][j] = e;
                     }
-                }
-                if (helper) {
-                    const T* rq = pl + (4 * ty + hrow + 2) * C3_PW + hqc;   // row of q in plane a
-                    const T c = rq[0];
-                    T e = acc_term<T, true>(E0, P.w7[1], rq[-C3_PW]);
-                    e = acc_term<T, true>(e, P.w7[2], rq[-1]);
-                    e = acc_term<T, true>(e, P.w7[3] - T(1), c);
-                    e = acc_term<T, true>(e, P.w7[4], rq[1]);
-                    e = acc_term<T, true>(e, P.w7[5], rq[C3_PW]);
-                    Eh = acc_term<T, true>(E1, P.w7[6], c);       // plane a-1 complete
-                    E1 = e;                                       // plane a: in-plane terms
-                    E0 = acc_first<T, true>(P.w7[0], c);          // plane a+1 starts
                 }
             }
             const int zc = p_first + t - 2;       // completed output plane

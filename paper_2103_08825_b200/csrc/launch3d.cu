@@ -151,6 +151,34 @@ void composed_star_weights(const sb_plan* P, T (&w)[125], T (&w7)[7]) {
     for (int i = 0; i < 7; i++) w7[i] = (T)P->weights[i];   // canonical star order
 }
 
+// Exact two-step weights of an x-face point p (x = 0: side 0, x = nx-1: side 1;
+// y, z off the shell): its neighbour q = p + s*e_x is the held halo, so
+// W_s(d) = sum over star pairs o + o' = d with o != s*e_x of w_o w_o', plus
+// w_{s e_x} at d = s*e_x (the halo value itself).  Long double, rounded once.
+template <typename T>
+void xface_weights(const sb_plan* P, T (&wx)[2][125]) {
+    long double s3[3][3][3] = {};
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[3 * i];
+        s3[o[0] + 1][o[1] + 1][o[2] + 1] = (long double)P->weights[i];
+    }
+    for (int side = 0; side < 2; side++) {
+        const int sx = side == 0 ? -1 : 1;
+        long double c[125] = {};
+        for (int a = 0; a < 27; a++) {
+            const int az = a / 9 - 1, ay = a / 3 % 3 - 1, axx = a % 3 - 1;
+            if (az == 0 && ay == 0 && axx == sx) continue;                 // the halo neighbour
+            for (int b = 0; b < 27; b++) {
+                const int bz = b / 9 - 1, by = b / 3 % 3 - 1, bx = b % 3 - 1;
+                const long double p = s3[az + 1][ay + 1][axx + 1] * s3[bz + 1][by + 1][bx + 1];
+                if (p != 0) c[sb::c3_widx(az + bz, ay + by, axx + bx)] += p;
+            }
+        }
+        c[sb::c3_widx(0, 0, sx)] += s3[1][1][sx + 1];
+        for (int i = 0; i < 125; i++) wx[side][i] = (T)c[i];
+    }
+}
+
 bool compose3d_ok(const sb_plan* P, int k) {
     static const int enabled = (int)env_double("SB200_3D_COMPOSE", 1);
     return enabled && k == 2 && (P->dtype == SB_F64 || enabled == 2) && P->shape == SB_STAR && P->arith == SB_ARITH_FMA && P->nw == 7 &&
@@ -204,7 +232,7 @@ int launch_compose3d(sb_plan* P, int src_idx) {
     prm.counter = P->d_counter;
     T w7[7];
     composed_star_weights<T>(P, prm.w, w7);
-    for (int i = 0; i < 7; i++) prm.w7[i] = w7[i];
+    xface_weights<T>(P, prm.wx);
 
     // physical shell on the side stream (disjoint points; both read only src)
     sb::Shell3DParams<T> sp;

@@ -279,6 +279,28 @@ def test_c5_full_size_fma():
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
 
 
+# --- non-finite values: NaN / Inf spread through exactly the oracle's cone
+
+@pytest.mark.parametrize("cfg,dims,k,arith", [
+    ("c2", (20000,), 32, "fma"), ("c2", (5000,), 8, "exact"), ("c3a", (40, 130), 4, "fma"),
+    ("c3b", (40, 130), 8, "exact"), ("c4", (12, 30, 70), 2, "fma"), ("c5", (10, 30, 66), 2, "fma"),
+])
+def test_nonfinite_propagation_matches_oracle(cfg, dims, k, arith):
+    spec = config_spec(cfg)
+    box = seeded_box(dims, spec.r, seed=3)
+    mid = tuple(n // 2 + spec.r for n in dims)
+    box[mid] = np.nan
+    edge = tuple(spec.r for _ in dims)                 # first interior point, next to the halo
+    box[edge] = np.inf
+    T = 2 * k + 1
+    got = sweep(spec, box, T, arith=arith, k=k)
+    want = oracle(spec, box, T)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    assert np.array_equal(np.isposinf(got), np.isposinf(want))
+    fin = np.isfinite(want)
+    assert np_oracle.max_rel_error(got[fin], want[fin]) <= FP64_TOL
+
+
 # --- range launches (slab edge planes first, interior later: sb_launch_range)
 
 @pytest.mark.parametrize("cfg,dims,k,arith", [
