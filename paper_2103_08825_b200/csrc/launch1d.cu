@@ -91,8 +91,9 @@ int launch_fused1d_k(sb_plan* P, const T* src, T* dst) {
         SB_CUDA(cudaFuncSetAttribute(ekern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (SH::IN_ELEMS + SH::OUT_ELEMS) * (int)sizeof(T)));
         SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Chunk1D) * chunks.size()));
-        SB_CUDA(cudaMemcpy(e.d_chunks, chunks.data(), sizeof(sb::Chunk1D) * chunks.size(),
-                           cudaMemcpyHostToDevice));
+        SB_CUDA(cudaMemcpyAsync(e.d_chunks, chunks.data(), sizeof(sb::Chunk1D) * chunks.size(),
+                           cudaMemcpyHostToDevice, P->stream));
+        SB_CUDA(cudaStreamSynchronize(P->stream));
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }

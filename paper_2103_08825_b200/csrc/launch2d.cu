@@ -100,7 +100,11 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
         e.comp_hi = y_hi;
         e.nchunks = (int)items.size();
         SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Item2D) * items.size()));
-        SB_CUDA(cudaMemcpy(e.d_chunks, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice));
+        // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and the
+        // kernel runs on the (non-blocking) plan stream
+        SB_CUDA(cudaMemcpyAsync(e.d_chunks, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice,
+                                P->stream));
+        SB_CUDA(cudaStreamSynchronize(P->stream));
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }

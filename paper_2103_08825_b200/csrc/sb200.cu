@@ -553,7 +553,9 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
         std::vector<float> wf(P->weights.begin(), P->weights.end());
         SB_CUDA_P(cudaMemcpy(P->d_w, wf.data(), 4 * P->nw, cudaMemcpyHostToDevice));
     }
-    SB_CUDA_P(cudaStreamSynchronize(P->stream));
+    // the setup above mixes the legacy stream (memset/memcpy) and the non-blocking
+    // plan stream: wait for both before any kernel can read these tables
+    SB_CUDA_P(cudaDeviceSynchronize());
 #undef SB_CUDA_P
     *out = P;
     return SB_OK;

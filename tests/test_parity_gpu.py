@@ -10,6 +10,8 @@
   properties (constant preservation, halo preservation, linearity).
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -447,6 +449,52 @@ def test_c3_full_size_fma(cfg):
     got = sweep(spec, box, 16, arith="fma", k=8)
     want = oracle(spec, box, 16)
     assert np_oracle.max_rel_error(got, want) <= FP64_TOL
+
+
+@pytest.mark.parametrize("cfg", ["c3a", "c3b"])
+def test_c3_full_size_exact(cfg):
+    # EXACT mode at the full BASELINE size: bit-identical to the oracle
+    spec = config_spec(cfg)
+    box = seeded_box((16384, 16384), 1, seed=9, halo="zero")
+    got = sweep(spec, box, 9, arith="exact", k=4)
+    assert got.tobytes() == oracle(spec, box, 9).tobytes()
+
+
+def test_c5_full_size_exact():
+    spec = config_spec("c5")
+    box = seeded_box((768, 768, 768), 1, seed=10)
+    got = sweep(spec, box, 3, arith="exact", k=2)
+    assert got.tobytes() == oracle(spec, box, 3).tobytes()
+
+
+FRESH_PROCESS_CHECK = r"""
+import sys, numpy as np
+sys.path[:0] = [%r, %r]
+from conftest import seeded_box
+from oracle import c_oracle
+from paper_2103_08825_b200.core import canonical, config_spec
+from paper_2103_08825_b200.plan import sweep
+for cfg, dims, k in (("c3a", (4096, 4096), 4), ("c2", (1 << 22,), 8), ("c5", (96, 130, 200), 2)):
+    spec = config_spec(cfg)
+    box = seeded_box(dims, spec.r, seed=1)
+    offs, ws = canonical(spec)
+    got = sweep(spec, box, 2 * k + 1, arith="exact", k=k)
+    want = c_oracle.sweep(box, spec.r, offs, ws, 2 * k + 1)
+    assert got.tobytes() == want.tobytes(), cfg
+print("fresh ok")
+"""
+
+
+def test_first_sweep_of_a_fresh_process_exact():
+    # regression: schedule tables were uploaded with a pageable cudaMemcpy on the
+    # legacy stream while the kernels run on a non-blocking stream -- the first
+    # sweep of a process could read a half-written schedule
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = FRESH_PROCESS_CHECK % (repo, os.path.join(repo, "tests"))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "fresh ok" in r.stdout, r.stderr[-2000:]
 
 
 def test_async_transfers_pipelined_two_plans():
