@@ -467,6 +467,42 @@ def test_c5_full_size_exact():
     assert got.tobytes() == oracle(spec, box, 3).tobytes()
 
 
+# --- seeded fuzz: random stencil class, extents, depth and T, EXACT = bit-identical
+
+FUZZ_CASES = []
+_frng = np.random.default_rng(20261020)
+for _i in range(36):
+    _d = int(_frng.integers(1, 4))
+    _cfg = {1: ["c1", "c2", "p:1d3p", "p:1d5p"], 2: ["c3a", "c3b", "p:2d5p", "p:2d9p"],
+            3: ["c4", "c5", "p:3d7p", "p:3d27p"]}[_d][int(_frng.integers(0, 4))]
+    if _d == 1:
+        _dims = (int(_frng.integers(16, 70000)),)
+        _k = int(_frng.choice([1, 2, 4, 8, 16]))
+    elif _d == 2:
+        _dims = (int(_frng.integers(3, 90)), int(_frng.integers(3, 700)))
+        _k = int(_frng.choice([1, 2, 4, 8]))
+    else:
+        _dims = (int(_frng.integers(3, 30)), int(_frng.integers(3, 50)), int(_frng.integers(3, 140)))
+        _k = int(_frng.integers(1, 5))
+    FUZZ_CASES.append((_cfg, _dims, _k, int(_frng.integers(1, 3 * _k + 3)), str(_frng.choice(["full", "zero"]))))
+
+
+@pytest.mark.parametrize("cfg,dims,k,T,halo", FUZZ_CASES)
+def test_fuzz_exact_bit_identical(cfg, dims, k, T, halo):
+    spec = make_stencil_spec(cfg[2:]) if cfg.startswith("p:") else config_spec(cfg)
+    box = seeded_box(dims, spec.r, seed=sum(dims) + k + T, halo=halo)
+    got = sweep(spec, box, T, arith="exact", k=k)
+    assert got.tobytes() == oracle(spec, box, T).tobytes()
+
+
+@pytest.mark.parametrize("cfg,dims,k,T,halo", FUZZ_CASES[::2])
+def test_fuzz_fma_within_bar(cfg, dims, k, T, halo):
+    spec = make_stencil_spec(cfg[2:]) if cfg.startswith("p:") else config_spec(cfg)
+    box = seeded_box(dims, spec.r, seed=sum(dims) + 2 * k + T, halo=halo)
+    got = sweep(spec, box, T, arith="fma", k=k)
+    assert np_oracle.max_rel_error(got, oracle(spec, box, T)) <= FP64_TOL
+
+
 FRESH_PROCESS_CHECK = r"""
 import sys, numpy as np
 sys.path[:0] = [%r, %r]
