@@ -526,8 +526,9 @@ def run_gpu_arm(args):
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels * world,
-            "gpu_launches_note": "all ranks; per sweep and rank: ceil(T/k) main launches + the "
-                                 "boundary / shell kernels on a side stream",
+            "gpu_launches_note": "all ranks; per sweep and rank: ceil(T/k) main launches (1D composed: "
+                                 "boundary windows inside the same launch) + the level-by-level tail's "
+                                 "boundary kernel / the 3D shell kernel on a side stream",
             "clocks": clocks.summary(),
         }
         if sweep is not None:

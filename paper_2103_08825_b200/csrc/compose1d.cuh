@@ -48,9 +48,92 @@ __device__ __forceinline__ int c1_pad(int i) {   // element index -> padded elem
     return i + (chunk / 4) * VEC;
 }
 
-template <typename T, int HALF>   // HALF = R*K
+// Exact level-by-level boundary windows for the composed path: one warp per
+// physical side advances the K steps over the window holding the dependency
+// cone of the E = RK outputs next to the boundary, with the Dirichlet halo
+// fixed at every level (HaloEdges, timejam.py:53-71) and the same
+// canonical-order arithmetic as every other kernel.  The window lives in
+// registers (lane l holds PER consecutive positions, neighbours arrive by
+// shuffles), so a level costs one shuffle round and 2R+1 dependent FMAs --
+// the window is on the critical path of short sweeps (C1: 64 levels).
+template <typename T, int R>
+struct EdgeWindowParams {
+    const T* src;      // interior position 0
+    T* dst;
+    int64_t n;
+    int side[2];       // per block: 0 = low side, 1 = high side
+    T w[2 * R + 1];
+};
+
+template <typename T, int R, int K, bool FMA>
+__device__ __forceinline__ void edge_window_body(const EdgeWindowParams<T, R> P, int b, int lane) {
+    constexpr int E = R * K;                        // outputs per side
+    constexpr int SPAN = 2 * E + R;                 // outputs + dependency cone + halo
+    constexpr int PER = (SPAN + 31) / 32 > R ? (SPAN + 31) / 32 : R;
+    const bool lo = P.side[b] == 0;
+    // low side: window [-R, 2E); high side: [n - 2E, n + R)
+    const int64_t first = lo ? -(int64_t)R : P.n - 2 * E;
+    T v[PER];
+    unsigned fixed = 0;                             // halo positions never change
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+        const int64_t pos = first + lane * PER + j;
+        v[j] = (pos >= -R && pos < P.n + R) ? P.src[pos] : T(0);
+        fixed |= (unsigned)(pos < 0 || pos >= P.n) << j;
+    }
+#pragma unroll 1
+    for (int step = 0; step < K; step++) {
+        // values beyond the window's two ends are garbage; it spreads R per
+        // level, i.e. at most RK positions deep -- never into the outputs
+        T left[R], right[R];
+#pragma unroll
+        for (int q = 0; q < R; q++) {
+            left[q] = __shfl_up_sync(0xffffffffu, v[PER - R + q], 1);
+            right[q] = __shfl_down_sync(0xffffffffu, v[q], 1);
+        }
+        T nv[PER];
+#pragma unroll
+        for (int j = 0; j < PER; j++) {
+            T acc = T(0);
+#pragma unroll
+            for (int t = 0; t <= 2 * R; t++) {
+                const int i = j - R + t;
+                const T x = i < 0 ? left[R + i] : (i >= PER ? right[i - PER] : v[i]);
+                acc = t == 0 ? acc_first<T, FMA>(P.w[0], x) : acc_term<T, FMA>(acc, P.w[t], x);
+            }
+            nv[j] = ((fixed >> j) & 1) ? v[j] : acc;
+        }
+#pragma unroll
+        for (int j = 0; j < PER; j++) v[j] = nv[j];
+    }
+    const int out0 = lo ? R : E;                    // window index of the first output
+#pragma unroll
+    for (int j = 0; j < PER; j++) {
+        const int i = lane * PER + j - out0;
+        const int64_t pos = first + lane * PER + j;
+        if (i >= 0 && i < E && pos >= 0 && pos < P.n) P.dst[pos] = v[j];
+    }
+}
+
+template <typename T, int R, int K, bool FMA>
+__global__ void __launch_bounds__(32)
+edge_window_kernel(const EdgeWindowParams<T, R> P) {
+    edge_window_body<T, R, K, FMA>(P, blockIdx.x, threadIdx.x);
+}
+
+// R > 0: the first `nedge` CTAs run the boundary windows (warp 0 each, exact
+// level by level) instead of composed tiles -- one launch per sweep step, no
+// side-stream fork/join; scheduled first, so they overlap the composed tiles.
+template <typename T, int HALF, int R = 0>   // HALF = R*K
 __global__ void __launch_bounds__(C1_WARPS * 32)
-compose1d_kernel(const Compose1DParams<T> P) {
+compose1d_kernel(const Compose1DParams<T> P, const EdgeWindowParams<T, (R > 0 ? R : 1)> EP = {}, int nedge = 0) {
+    if constexpr (R > 0) {
+        if ((int)blockIdx.x < nedge) {
+            if (threadIdx.x < 32) edge_window_body<T, R, HALF / R, true>(EP, blockIdx.x, threadIdx.x);
+            return;
+        }
+    }
+    const int bid = (int)blockIdx.x - (R > 0 ? nedge : 0);
     constexpr int VEC = Vec16<T>::n;
     constexpr int TILE = 32 * C1_B;
     constexpr int SPAN = TILE + 2 * HALF;                 // inputs per tile
@@ -68,7 +151,7 @@ compose1d_kernel(const Compose1DParams<T> P) {
     // before the current tile's FMAs and its result is read after them (no
     // claim at all when the static tiles cover the line, e.g. C1).
     // (volatile asm keeps the compiler from sinking the atomic next to its use)
-    const int64_t gw = (int64_t)blockIdx.x * C1_WARPS + warp;
+    const int64_t gw = (int64_t)bid * C1_WARPS + warp;
     const int64_t tw = P.total_warps;
     const bool dynamic = P.ntiles > 2 * tw;
     auto claim_issue = [&]() -> unsigned {
@@ -143,75 +226,6 @@ compose1d_kernel(const Compose1DParams<T> P) {
             atomicExch(&P.counter[2], 0u);
             atomicExch(&P.counter[3], 0u);
         }
-    }
-}
-
-// Exact level-by-level boundary windows for the composed path: one warp per
-// physical side advances the K steps over the window holding the dependency
-// cone of the E = RK outputs next to the boundary, with the Dirichlet halo
-// fixed at every level (HaloEdges, timejam.py:53-71) and the same
-// canonical-order arithmetic as every other kernel.  The window lives in
-// registers (lane l holds PER consecutive positions, neighbours arrive by
-// shuffles), so a level costs one shuffle round and 2R+1 dependent FMAs --
-// the window is on the critical path of short sweeps (C1: 64 levels).
-template <typename T, int R>
-struct EdgeWindowParams {
-    const T* src;      // interior position 0
-    T* dst;
-    int64_t n;
-    int side[2];       // per block: 0 = low side, 1 = high side
-    T w[2 * R + 1];
-};
-
-template <typename T, int R, int K, bool FMA>
-__global__ void __launch_bounds__(32)
-edge_window_kernel(const EdgeWindowParams<T, R> P) {
-    constexpr int E = R * K;                        // outputs per side
-    constexpr int SPAN = 2 * E + R;                 // outputs + dependency cone + halo
-    constexpr int PER = (SPAN + 31) / 32 > R ? (SPAN + 31) / 32 : R;
-    const int lane = threadIdx.x;
-    const bool lo = P.side[blockIdx.x] == 0;
-    // low side: window [-R, 2E); high side: [n - 2E, n + R)
-    const int64_t first = lo ? -(int64_t)R : P.n - 2 * E;
-    T v[PER];
-    unsigned fixed = 0;                             // halo positions never change
-#pragma unroll
-    for (int j = 0; j < PER; j++) {
-        const int64_t pos = first + lane * PER + j;
-        v[j] = (pos >= -R && pos < P.n + R) ? P.src[pos] : T(0);
-        fixed |= (unsigned)(pos < 0 || pos >= P.n) << j;
-    }
-#pragma unroll 1
-    for (int step = 0; step < K; step++) {
-        // values beyond the window's two ends are garbage; it spreads R per
-        // level, i.e. at most RK positions deep -- never into the outputs
-        T left[R], right[R];
-#pragma unroll
-        for (int q = 0; q < R; q++) {
-            left[q] = __shfl_up_sync(0xffffffffu, v[PER - R + q], 1);
-            right[q] = __shfl_down_sync(0xffffffffu, v[q], 1);
-        }
-        T nv[PER];
-#pragma unroll
-        for (int j = 0; j < PER; j++) {
-            T acc = T(0);
-#pragma unroll
-            for (int t = 0; t <= 2 * R; t++) {
-                const int i = j - R + t;
-                const T x = i < 0 ? left[R + i] : (i >= PER ? right[i - PER] : v[i]);
-                acc = t == 0 ? acc_first<T, FMA>(P.w[0], x) : acc_term<T, FMA>(acc, P.w[t], x);
-            }
-            nv[j] = ((fixed >> j) & 1) ? v[j] : acc;
-        }
-#pragma unroll
-        for (int j = 0; j < PER; j++) v[j] = nv[j];
-    }
-    const int out0 = lo ? R : E;                    // window index of the first output
-#pragma unroll
-    for (int j = 0; j < PER; j++) {
-        const int i = lane * PER + j - out0;
-        const int64_t pos = first + lane * PER + j;
-        if (i >= 0 && i < E && pos >= 0 && pos < P.n) P.dst[pos] = v[j];
     }
 }
 

@@ -171,7 +171,8 @@ int launch_compose1d_k(sb_plan* P, const T* src, T* dst) {
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }
-    if (sc->nedge > 0) {   // boundary windows: exact level-by-level, side stream
+    static const int fuse_edges = (int)env_double("SB200_1D_FUSED_EDGES", 1);
+    if (sc->nedge > 0 && !fuse_edges) {   // boundary windows: exact level-by-level, side stream
         sb::EdgeWindowParams<T, R> ep;
         ep.src = src + P->g.origin;
         ep.dst = dst + P->g.origin;
@@ -199,6 +200,31 @@ int launch_compose1d_k(sb_plan* P, const T* src, T* dst) {
     cp.taps = 2 * HALF + 1;
     for (int i = 0; i < 2 * HALF + 1; i++) cp.c[i] = (T)sc->cw[i];
     P->last_kernel = "compose1d_kernel";
+    if (sc->nedge > 0 && fuse_edges) {
+        // boundary windows in the same launch: `nedge` leading CTAs; the composed grid
+        // shrinks by as many so the whole launch stays resident
+        sb::EdgeWindowParams<T, R> ep;
+        ep.src = src + P->g.origin;
+        ep.dst = dst + P->g.origin;
+        ep.n = n;
+        int b = 0;
+        if (P->phys_lo) ep.side[b++] = 0;
+        if (P->phys_hi) ep.side[b++] = 1;
+        for (int i = 0; i < 2 * R + 1; i++) ep.w[i] = (T)P->weights[i];
+        const int main_blocks = std::max(1, sc->blocks - sc->nedge);
+        cp.total_warps = main_blocks * sb::C1_WARPS;
+        auto ck = sb::compose1d_kernel<T, HALF, R>;
+        static bool attr_set = false;   // per instantiation
+        if (!attr_set) {
+            SB_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         sb::compose1d_smem_bytes<T, HALF>()));
+            attr_set = true;
+        }
+        ck<<<(unsigned)(main_blocks + sc->nedge), sb::C1_WARPS * 32, sb::compose1d_smem_bytes<T, HALF>(), P->stream>>>(
+            cp, ep, sc->nedge);
+        SB_CUDA(cudaGetLastError());
+        return SB_OK;
+    }
     if (cp.ntiles > 0) {
         sb::compose1d_kernel<T, HALF><<<(unsigned)sc->blocks, sb::C1_WARPS * 32,
             sb::compose1d_smem_bytes<T, HALF>(), P->stream>>>(cp);

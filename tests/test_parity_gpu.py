@@ -213,7 +213,7 @@ def test_c1_full_size_one_launch_k64():
         p.upload(box)
         t = p.run(64)
         got = p.download()
-    assert t.launches == 2 and t.kernel_name == "compose1d_kernel"   # composed + boundary windows
+    assert t.launches == 1 and t.kernel_name == "compose1d_kernel"   # composed + boundary windows, one launch
     assert np_oracle.max_rel_error(got, oracle(spec, box, 64)) <= FP64_TOL
 
 
