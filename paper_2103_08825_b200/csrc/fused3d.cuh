@@ -41,7 +41,7 @@ namespace sb {
 constexpr int F3_CW = 64;        // computed region width (x)
 constexpr int F3_PW = 68;        // shared plane width: ring + region + pad (16 B rows)
 #ifndef SB_F3_NS0
-#define SB_F3_NS0 4
+#define SB_F3_NS0 3     // measured: 3 >= 4 > 2 on every C4/C5 depth (C5 fp32 k=2 +4%, fp64 +1-2%)
 #endif
 #ifndef SB_F3_DBL
 #define SB_F3_DBL 0     // double-buffered level planes: no end-of-plane barrier
