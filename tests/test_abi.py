@@ -83,3 +83,36 @@ def test_null_arguments(lib):
     assert lib.sb_plan_create(None, None) == _abi.SB_ERR_ARG
     assert lib.sb_run(None, 1, None) == _abi.SB_ERR_ARG
     assert lib.sb_upload(None, None, 0) == _abi.SB_ERR_ARG
+
+
+def _build_c_client(tmp_path):
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no C compiler")
+    exe = str(tmp_path / "sweep_c1")
+    libdir = os.path.join(REPO, "paper_2103_08825_b200", "lib")
+    r = subprocess.run([gcc, "-O2", "-ffp-contract=off", "-Wall", "-I", os.path.join(REPO, "include"),
+                        os.path.join(REPO, "examples", "sweep_c1.c"), "-L", libdir, "-lsb200",
+                        f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+def test_c_client_builds_and_fails_loudly_without_device(lib, tmp_path):
+    # the C ABI is usable from plain C; without a GPU every compute call fails with SB_ERR_CUDA
+    import subprocess
+    if lib.sb_device_count() > 0:
+        pytest.skip("a device is present")
+    exe = _build_c_client(tmp_path)
+    r = subprocess.run([exe, "100", "3"], capture_output=True, text=True)
+    assert r.returncode == 2 and "no CUDA device" in r.stderr
+
+
+@pytest.mark.gpu
+def test_c_client_bit_identical_on_device(lib, tmp_path):
+    import subprocess
+    exe = _build_c_client(tmp_path)
+    r = subprocess.run([exe, "300007", "37"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.startswith("bit-identical"), r.stdout + r.stderr
