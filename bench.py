@@ -264,7 +264,7 @@ def kernel_label(spec, wl, k, arith):
     """Main kernel a sweep of this workload launches (see sb200.cu / launch*.cu)."""
     d = len(wl["dims"])
     if d == 1:
-        return (f"compose1d_kernel<double, {spec.r * k}>" if arith == "fma" and k >= 16
+        return (f"compose1d_kernel<double, {spec.r * k}, {spec.r}>" if arith == "fma" and k >= 16
                 else f"fused1d_kernel (K={k})")
     if d == 2:
         return f"fused2d_kernel (K={k})"
