@@ -6,6 +6,7 @@
 
 #include "plan.hpp"
 #include "fused2d.cuh"
+#include "sep2d.cuh"
 
 namespace sbh {
 namespace {
@@ -173,9 +174,133 @@ int launch_fused2d_t(sb_plan* P, const T* src, T* dst, int k) {
 }
 
 
+// ---- separable composed path (sep2d.cuh)
+
+std::vector<long double> conv_power(const long double w[3], int K) {
+    std::vector<long double> c(1, 1.0L);
+    for (int s = 0; s < K; s++) {
+        std::vector<long double> n(c.size() + 2, 0.0L);
+        for (size_t i = 0; i < c.size(); i++)
+            for (int j = 0; j < 3; j++) n[i + j] += c[i] * w[j];
+        c.swap(n);
+    }
+    return c;
+}
+
+std::vector<sb::BandItem> band_items(int64_t ny, int64_t nx, int K) {
+    std::vector<sb::BandItem> out;
+    const int W = sb::SEP_BW;
+    for (int64_t x = 0; x < nx; x += W) {                  // top / bottom bands: K rows, all columns
+        const int w = (int)std::min<int64_t>(W, nx - x);
+        out.push_back({0, (int32_t)x, K, w});
+        out.push_back({(int32_t)(ny - K), (int32_t)x, K, w});
+    }
+    for (int64_t y = K; y < ny - K; y += W) {              // left / right bands: K columns
+        const int h = (int)std::min<int64_t>(W, ny - K - y);
+        out.push_back({(int32_t)y, 0, h, K});
+        out.push_back({(int32_t)y, (int32_t)(nx - K), h, K});
+    }
+    return out;
+}
+
+template <typename T, int K>
+int launch_sep2d_k(sb_plan* P, int src_idx) {
+    double a[3], b[3];
+    separable_weights(P, a, b);
+    const int64_t ny = P->dims[0], nx = P->dims[1];
+    if (!P->tmp) {
+        cudaError_t e = cudaMalloc(&P->tmp, P->buf_elems * P->es);
+        if (e != cudaSuccess) return fail(e == cudaErrorMemoryAllocation ? SB_ERR_NOMEM : SB_ERR_CUDA,
+                                          "separable scratch allocation failed: %s", cudaGetErrorString(e));
+    }
+    const int64_t origin = P->g.origin;
+    sb::SepParams<T> vp, hp;
+    vp.src = reinterpret_cast<const T*>(P->buf[src_idx]) + origin;
+    vp.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]) + origin;
+    vp.tmp = reinterpret_cast<T*>(P->tmp) + origin;
+    vp.sy = P->g.sy;
+    vp.nx = (int)nx;
+    vp.ny = (int)ny;
+    hp = vp;
+    const long double la[3] = {a[0], a[1], a[2]}, lb[3] = {b[0], b[1], b[2]};
+    const auto ca = conv_power(la, K), cb = conv_power(lb, K);
+    for (int i = 0; i < 2 * K + 1; i++) {
+        vp.c[i] = (T)ca[i];
+        hp.c[i] = (T)cb[i];
+    }
+    // band regions (cached per plan and depth; key -4000 - K)
+    Sched1D* sc = nullptr;
+    for (auto& e : P->sched1d)
+        if (e.K == -4000 - K) sc = &e;
+    if (!sc) {
+        auto items = band_items(ny, nx, K);
+        Sched1D e;
+        e.K = -4000 - K;
+        e.nchunks = (int)items.size();
+        SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::BandItem) * items.size()));
+        SB_CUDA(cudaMemcpyAsync(e.d_chunks, items.data(), sizeof(sb::BandItem) * items.size(),
+                                cudaMemcpyHostToDevice, P->stream));
+        SB_CUDA(cudaStreamSynchronize(P->stream));
+        const int smem = sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW);
+        SB_CUDA(cudaFuncSetAttribute(sb::sep_band_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        P->sched1d.push_back(e);
+        sc = &P->sched1d.back();
+    }
+    sb::SepBandParams<T> bp;
+    bp.src = vp.src;
+    bp.dst = vp.dst;
+    bp.sy = P->g.sy;
+    bp.nx = (int)nx;
+    bp.ny = (int)ny;
+    bp.items = reinterpret_cast<const sb::BandItem*>(sc->d_chunks);
+    bp.nitems = sc->nchunks;
+    for (int i = 0; i < 9; i++) bp.w[i] = T(0);
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[2 * i];
+        bp.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
+    }
+    // band: side stream, concurrent with the two passes (disjoint outputs)
+    SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
+    SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
+    sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
+                                P->side_stream>>>(bp);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+    dim3 vg((unsigned)((nx + sb::SEP_VT - 1) / sb::SEP_VT), (unsigned)((ny - 2 * K + sb::SEP_VB - 1) / sb::SEP_VB));
+    sb::sep_vpass_kernel<T, K><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
+    SB_CUDA(cudaGetLastError());
+    constexpr int TILE = 32 * sb::SEP_HB;
+    const int64_t tiles = (nx - 2 * K + TILE - 1) / TILE;
+    dim3 hg((unsigned)((tiles + sb::SEP_HW - 1) / sb::SEP_HW), (unsigned)(ny - 2 * K));
+    sb::sep_hpass_kernel<T, K><<<hg, sb::SEP_HW * 32, 0, P->stream>>>(hp);
+    SB_CUDA(cudaGetLastError());
+    SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
+    P->kernels_launched += 2;   // + the vertical pass counted by launch_one
+    P->last_kernel = "sep2d (vertical + horizontal composed passes)";
+    return SB_OK;
+}
+
+template <typename T>
+int launch_sep2d(sb_plan* P, int src_idx, int k) {
+    if (k == 16) return launch_sep2d_k<T, 16>(P, src_idx);
+    return launch_sep2d_k<T, 32>(P, src_idx);
+}
+
 }  // namespace
 
+bool sep2d_ok(const sb_plan* P, int k) {
+    static const int enabled = (int)env_double("SB200_SEP2D", 1);
+    double a[3], b[3];
+    return enabled && (k == 16 || k == 32) && P->d == 2 && P->phys_lo && P->phys_hi && P->zr_hi < 0 &&
+           P->dims[0] > 2 * k && P->dims[1] > 2 * k && separable_weights(P, a, b);
+}
+
 int launch_fused2d(sb_plan* P, int src_idx, int k) {
+    if (k >= 16) {
+        if (!sep2d_ok(P, k)) return fail(SB_ERR_ARG, "2D depth %d needs the separable composed path", k);
+        if (P->dtype == SB_F64) return launch_sep2d<double>(P, src_idx, k);
+        return launch_sep2d<float>(P, src_idx, k);
+    }
     const bool fma = P->arith == SB_ARITH_FMA;
     if (P->dtype == SB_F64) {
         auto src = reinterpret_cast<const double*>(P->buf[src_idx]);

@@ -89,6 +89,7 @@ struct sb_plan {
     std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
     CUtensorMap tmap[4][2];                // TMA descriptors [geometry][buffer] (3D; 2, 3: composed)
     bool tmap_ok[4] = {false, false, false, false};
+    void* tmp = nullptr;                   // scratch grid of the separable composed 2D path
     void* stage = nullptr;                 // reference-storage staging rows (sb_upload_storage)
     size_t stage_bytes = 0;
     int64_t stage_row_elems = 0;
@@ -116,6 +117,7 @@ int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
 int make_tensor_maps(sb_plan* P, int geo, int box_h);
 int finish_upload(sb_plan* P);   // buf[0] uploaded: mirror halo/ghost into buf[1], make buf[0] current
+bool sep2d_ok(const sb_plan* P, int k);   // launch2d.cu: separable composed 2D path serves depth k
 inline int64_t range_lo(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_lo : 0; }
 inline int64_t range_hi(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_hi : P->dims[0]; }
 

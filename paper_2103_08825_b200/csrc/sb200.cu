@@ -110,7 +110,7 @@ int fused_kind(const sb_plan* P) {
 // Supported fused depths (template instantiations) per kernel.
 bool fused_k_ok(const sb_plan* P, int kind, int k) {
     if (kind == KK_FUSED3D) return k >= 1 && k <= 4;
-    if (kind == KK_FUSED2D) return k == 1 || k == 2 || k == 4 || k == 8;
+    if (kind == KK_FUSED2D) return k == 1 || k == 2 || k == 4 || k == 8 || ((k == 16 || k == 32) && sep2d_ok(P, k));
     if (k == 32 || k == 64) return compose1d_ok(P, k, 16);   // composed path only
     return k == 1 || k == 2 || k == 4 || k == 8 || k == 16;
 }
@@ -124,7 +124,13 @@ int largest_fused_k(int kind, int64_t steps, int kmax) {
 
 int default_k(int kind, const sb_plan* P) {
     if (kind == KK_FUSED3D) return 2;   // measured best for both 3D stencils (C4, C5)
-    if (kind == KK_FUSED2D) return 4;   // measured best on C3 (k=4: ~800, k=8: ~710 GStencil/s)
+    if (kind == KK_FUSED2D) {
+        // rank-1 weights in FMA mode: the separable composed path (K2c); else the
+        // level-by-level kernel's measured best (C3 k=4)
+        const int ks = (int)env_double("SB200_SEP2D_K", 32);
+        if ((ks == 16 || ks == 32) && sep2d_ok(P, ks)) return ks;
+        return 4;
+    }
     // 1D: the deepest composed depth in FMA mode (C2 k=32: ~3960 vs k=16: ~3670;
     // C1 k=64: one launch for T=64), else the level-by-level kernel's 16
     if (compose1d_ok(P, 64, 16)) return 64;
@@ -384,6 +390,7 @@ void sb_plan_destroy(sb_plan* P) {
     if (P->d_counter) cudaFree(P->d_counter);
     if (P->d_trace) cudaFree(P->d_trace);
     if (P->stage) cudaFree(P->stage);
+    if (P->tmp) cudaFree(P->tmp);
     for (auto& e : P->sched1d)
         if (e.d_chunks) cudaFree(e.d_chunks);
     for (auto& g : P->graphs)

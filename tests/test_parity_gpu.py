@@ -343,6 +343,70 @@ def test_separable2d_within_fp64_bar(k, dims):
         assert np_oracle.max_rel_error(got, oracle(spec, box, T)) <= FP64_TOL
 
 
+# --- separable composed 2D (FMA, rank-1 weights, K = 16 / 32 as two 1D passes + exact bands)
+
+@pytest.mark.parametrize("k", [16, 32])
+@pytest.mark.parametrize("dims", [(2 * 32 + 1, 2 * 32 + 1), (77, 300), (400, 1037), (1000, 513)])
+@pytest.mark.parametrize("halo", ["full", "zero"])
+def test_sep2d_composed_within_fp64_bar(k, dims, halo):
+    from paper_2103_08825_b200.core import StencilSpec
+    if min(dims) <= 2 * k:
+        pytest.skip("grid too small for the composed depth")
+    a, b = np.array([0.2, 0.5, 0.3]), np.array([0.15, 0.6, 0.25])
+    w = {(dy, dx): float(a[dy + 1] * b[dx + 1]) for dy in (-1, 0, 1) for dx in (-1, 0, 1)}
+    for spec in (config_spec("c3a"), StencilSpec("rank1", 2, 1, "box", w)):
+        box = seeded_box(dims, 1, seed=sum(dims) + k, halo=halo)
+        if halo == "full":                       # halo values far from the interior's
+            box[0], box[-1], box[:, 0], box[:, -1] = 3.0, -2.0, 5.0, 0.25
+        T = 2 * k + 5                            # two composed launches + a level-by-level tail
+        with Plan(spec, dims, k=k, arith="fma") as p:
+            p.upload(box)
+            t = p.run(T)
+            got = p.download()
+        assert t.kernel_name.startswith("sep2d") or t.kernel_name == "fused2d_kernel"
+        want = oracle(spec, box, T)
+        assert np_oracle.max_rel_error(interior(got, 1), interior(want, 1)) <= FP64_TOL
+        mask = np.ones(box.shape, bool)
+        mask[1:-1, 1:-1] = False
+        assert np.array_equal(got[mask], box[mask])
+
+
+def test_sep2d_is_the_default_for_rank1_fma_and_not_exact():
+    spec = config_spec("c3a")
+    with Plan(spec, (300, 400), arith="fma") as p:
+        assert p.k in (16, 32)
+    with Plan(spec, (300, 400), arith="exact") as p:
+        assert p.k == 4
+    with Plan(config_spec("c3b"), (300, 400), arith="fma") as p:
+        assert p.k == 4
+
+
+def test_sep2d_nonfinite_propagation():
+    spec = config_spec("c3a")
+    dims = (200, 300)
+    box = seeded_box(dims, 1, seed=3)
+    box[100, 150] = np.nan
+    box[1, 1] = np.inf
+    box[150, 3] = np.inf
+    got = sweep(spec, box, 32, arith="fma", k=16)
+    want = oracle(spec, box, 32)
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    assert np.array_equal(np.isposinf(got), np.isposinf(want))
+    fin = np.isfinite(want)
+    assert np_oracle.max_rel_error(got[fin], want[fin]) <= FP64_TOL
+
+
+def test_c3a_full_size_sep2d():
+    spec = config_spec("c3a")
+    box = seeded_box((16384, 16384), 1, seed=12)
+    with Plan(spec, (16384, 16384), arith="fma") as p:
+        p.upload(box)
+        t = p.run(40)
+        got = p.download()
+    assert t.kernel_name.startswith("sep2d") or t.k_used >= 16
+    assert np_oracle.max_rel_error(got, oracle(spec, box, 40)) <= FP64_TOL
+
+
 # --- composed 3D star (FMA, k=2 as one 25-point pass + exact physical shell)
 
 @pytest.mark.parametrize("dims", [(4, 4, 4), (5, 9, 7), (9, 40, 70), (37, 33, 130), (20, 17, 131)])
