@@ -266,8 +266,24 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
                                 P->side_stream>>>(bp);
     SB_CUDA(cudaGetLastError());
     SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
-    dim3 vg((unsigned)((nx + sb::SEP_VT - 1) / sb::SEP_VT), (unsigned)((ny - 2 * K + sb::SEP_VB - 1) / sb::SEP_VB));
-    sb::sep_vpass_kernel<T, K><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
+    // staged vertical pass at K = 32 (C3a 2492 -> 2778); at K = 16 the direct one
+    // measured faster (1881 vs 1449)
+    static const int vsmem = (int)env_double("SB200_SEP2D_VSMEM", 1);
+    if (vsmem && K == 32) {
+        constexpr int OUT = sb::SEP_VW * sb::SEP_VB;
+        const int smem = sb::sep_vpass_smem_bytes<T, K>();
+        static bool attr = false;
+        if (!attr) {
+            SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem));
+            attr = true;
+        }
+        dim3 vg((unsigned)((nx + 31) / 32), (unsigned)((ny - 2 * K + OUT - 1) / OUT));
+        sb::sep_vpass_smem_kernel<T, K><<<vg, sb::SEP_VW * 32, smem, P->stream>>>(vp);
+    } else {
+        dim3 vg((unsigned)((nx + sb::SEP_VT - 1) / sb::SEP_VT), (unsigned)((ny - 2 * K + sb::SEP_VB - 1) / sb::SEP_VB));
+        sb::sep_vpass_kernel<T, K><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
+    }
     SB_CUDA(cudaGetLastError());
     constexpr int TILE = 32 * sb::SEP_HB;
     const int64_t tiles = (nx - 2 * K + TILE - 1) / TILE;

@@ -26,12 +26,18 @@
 
 namespace sb {
 
-constexpr int SEP_VB = 16;         // output rows per thread in the vertical pass
+#ifndef SB_SEP_VB
+#define SB_SEP_VB 16
+#endif
+#ifndef SB_SEP_HB
+#define SB_SEP_HB 8
+#endif
+constexpr int SEP_VB = SB_SEP_VB;  // output rows per thread in the vertical pass
 constexpr int SEP_VT = 128;        // threads per vertical-pass CTA (columns)
-constexpr int SEP_HB = 8;          // outputs per lane in the horizontal pass
+constexpr int SEP_HB = SB_SEP_HB;  // outputs per lane in the horizontal pass
 constexpr int SEP_HW = 4;          // warps per horizontal-pass CTA
 constexpr int SEP_BW = 64;         // band chunk width (outputs along the band)
-constexpr int SEP_BT = 256;        // band CTA threads
+constexpr int SEP_BT = 512;        // band CTA threads
 
 template <typename T>
 struct SepParams {
@@ -64,6 +70,47 @@ __global__ void __launch_bounds__(SEP_VT) sep_vpass_kernel(const SepParams<T> P)
 #pragma unroll
     for (int o = 0; o < SEP_VB; o++)
         if (y0 + o < P.ny - K) d[(int64_t)o * P.sy] = acc[o];
+}
+
+// Shared-memory staged form of the vertical pass: a CTA of SEP_VW warps owns 32
+// columns x (SEP_VW * SEP_VB) output rows and loads its 2K + SEP_VW*SEP_VB input
+// rows once (coalesced 256 B row segments), so L2 traffic per output is
+// (2K + VW*VB) / (VW*VB) elements instead of (2K + VB) / VB.
+constexpr int SEP_VW = 8;
+template <typename T, int K>
+constexpr int sep_vpass_smem_bytes() { return (2 * K + SEP_VW * SEP_VB) * 32 * (int)sizeof(T); }
+
+template <typename T, int K>
+__global__ void __launch_bounds__(SEP_VW * 32) sep_vpass_smem_kernel(const SepParams<T> P) {
+    extern __shared__ __align__(16) unsigned char smem_v[];
+    T* col = reinterpret_cast<T*>(smem_v);            // [row][32]
+    constexpr int ROWS = 2 * K + SEP_VW * SEP_VB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int x = blockIdx.x * 32 + lane;
+    const int yb = K + blockIdx.y * (SEP_VW * SEP_VB);  // first output row of the CTA
+    const int y_end = P.ny - K;
+    for (int r = warp; r < ROWS; r += SEP_VW) {
+        const int y = yb - K + r;                       // input row (<= ny - 1 + ... guarded)
+        col[r * 32 + lane] = (x < P.nx && y < P.ny + 1) ? P.src[(int64_t)y * P.sy + x] : T(0);
+    }
+    __syncthreads();
+    const int y0 = yb + warp * SEP_VB;
+    if (x >= P.nx || y0 >= y_end) return;
+    const T* s = col + warp * SEP_VB * 32 + lane;
+    T acc[SEP_VB];
+#pragma unroll
+    for (int m = 0; m < 2 * K + SEP_VB; m++) {
+        const T v = s[m * 32];
+#pragma unroll
+        for (int o = 0; o < SEP_VB; o++) {
+            const int t = m - o;
+            if (t >= 0 && t <= 2 * K) acc[o] = t == 0 ? v * P.c[0] : __fma_rn(P.c[t], v, acc[o]);
+        }
+    }
+    T* d = P.tmp + (int64_t)y0 * P.sy + x;
+#pragma unroll
+    for (int o = 0; o < SEP_VB; o++)
+        if (y0 + o < y_end) d[(int64_t)o * P.sy] = acc[o];
 }
 
 // dst[y][x] = sum_m b^{*K}[m] tmp[y][x+m], rows [K, ny-K), columns [K, nx-K).
@@ -164,21 +211,36 @@ __global__ void __launch_bounds__(SEP_BT) sep_band_kernel(const SepBandParams<T>
     // updatable cells: inside the interior and not on the region's outer ring
     const int ly_lo = max(1, -ry0), ly_hi = min(RH - 1, P.ny - ry0);
     const int lx_lo = max(1, -rx0), lx_hi = min(RW - 1, P.nx - rx0);
+    // work units: (32-column group, SEG-row segment); a lane walks its column down
+    // the segment with a 3 x 3 register window (3 shared loads per cell, not 9)
+    constexpr int SEG = 8;
+    const int ncg = (lx_hi - lx_lo + 31) / 32, nseg = (ly_hi - ly_lo + SEG - 1) / SEG;
     for (int l = 0; l < K; l++) {
-        for (int ly = ly_lo + warp; ly < ly_hi; ly += SEP_BT / 32)
-        for (int lx = lx_lo + lane; lx < lx_hi; lx += 32) {
-            const int i = ly * RW + lx;
-            const T* c = A + i;
-            T s = c[-RW - 1] * P.w[0];
-            s = __fma_rn(P.w[1], c[-RW], s);
-            s = __fma_rn(P.w[2], c[-RW + 1], s);
-            s = __fma_rn(P.w[3], c[-1], s);
-            s = __fma_rn(P.w[4], c[0], s);
-            s = __fma_rn(P.w[5], c[1], s);
-            s = __fma_rn(P.w[6], c[RW - 1], s);
-            s = __fma_rn(P.w[7], c[RW], s);
-            s = __fma_rn(P.w[8], c[RW + 1], s);
-            B[i] = s;
+        for (int u = warp; u < ncg * nseg; u += SEP_BT / 32) {
+            const int lx = lx_lo + (u % ncg) * 32 + lane;
+            const int r0 = ly_lo + (u / ncg) * SEG, r1 = min(ly_hi, r0 + SEG);
+            if (lx < lx_hi) {
+                const T* c = A + (r0 - 1) * RW + lx;
+                T a0 = c[-1], a1 = c[0], a2 = c[1];
+                c += RW;
+                T b0 = c[-1], b1 = c[0], b2 = c[1];
+                for (int ly = r0; ly < r1; ly++) {
+                    c += RW;
+                    const T d0 = c[-1], d1 = c[0], d2 = c[1];
+                    T s = a0 * P.w[0];
+                    s = __fma_rn(P.w[1], a1, s);
+                    s = __fma_rn(P.w[2], a2, s);
+                    s = __fma_rn(P.w[3], b0, s);
+                    s = __fma_rn(P.w[4], b1, s);
+                    s = __fma_rn(P.w[5], b2, s);
+                    s = __fma_rn(P.w[6], d0, s);
+                    s = __fma_rn(P.w[7], d1, s);
+                    s = __fma_rn(P.w[8], d2, s);
+                    B[ly * RW + lx] = s;
+                    a0 = b0, a1 = b1, a2 = b2;
+                    b0 = d0, b1 = d1, b2 = d2;
+                }
+            }
         }
         __syncthreads();
         T* t = A;
