@@ -161,11 +161,31 @@ __global__ void __launch_bounds__(SEP_HW * 32) sep_hpass_kernel(const SepParams<
             }
         }
     }
-    T* d = P.dst + (int64_t)y * P.sy;
-    const int xo = x0 + lane * SEP_HB;
+    // outputs through the (now free) staging buffer: each store instruction then
+    // writes a contiguous 32 x 16 B row segment (whole sectors) instead of 32
+    // lane-strided pieces
+    __syncwarp();
 #pragma unroll
-    for (int o = 0; o < SEP_HB; o++)
-        if (xo + o < P.nx - K) d[xo + o] = acc[o];
+    for (int v = 0; v < SEP_HB / VEC; v++) {
+        V pack;
+#pragma unroll
+        for (int e = 0; e < VEC; e++) reinterpret_cast<T*>(&pack)[e] = acc[v * VEC + e];
+        *reinterpret_cast<V*>(buf + c1_pad<T>(lane * SEP_HB + v * VEC)) = pack;
+    }
+    __syncwarp();
+    T* d = P.dst + (int64_t)y * P.sy + x0;
+    const int nout = P.nx - K - x0;                               // outputs of this tile inside the range
+#pragma unroll
+    for (int c = lane; c < TILE / VEC; c += 32) {
+        const V pack = *reinterpret_cast<const V*>(buf + c1_pad<T>(c * VEC));
+        if ((c + 1) * VEC <= nout) {
+            *reinterpret_cast<V*>(d + c * VEC) = pack;
+        } else {
+#pragma unroll
+            for (int e = 0; e < VEC; e++)
+                if (c * VEC + e < nout) d[c * VEC + e] = reinterpret_cast<const T*>(&pack)[e];
+        }
+    }
 }
 
 // One band region: outputs [oy0, oy0+oh) x [ox0, ox0+ow) (interior coordinates),
