@@ -23,6 +23,9 @@
 
 namespace sb {
 
+#ifndef SB_C1_COALESCED_STORES
+#define SB_C1_COALESCED_STORES 1
+#endif
 constexpr int C1_B = 8;          // outputs per lane per tile
 constexpr int C1_WARPS = 4;
 constexpr int C1_MAXTAPS = 129;  // R*K <= 64
@@ -199,7 +202,24 @@ compose1d_kernel(const Compose1DParams<T> P, const EdgeWindowParams<T, (R > 0 ? 
             }
         }
         const int64_t q0 = P.lo + tile * TILE + lane * C1_B;
-        if (q0 + C1_B <= P.hi) {
+        const int64_t t0 = P.lo + tile * TILE;
+        if (SB_C1_COALESCED_STORES && t0 + TILE <= P.hi) {
+            // whole tile: outputs through the tile's (consumed) staging buffer, so each
+            // store instruction writes a contiguous 512 B segment (whole sectors)
+            T* sb = const_cast<T*>(s);
+            __syncwarp();
+#pragma unroll
+            for (int v = 0; v < C1_B / VEC; v++) {
+                V pack;
+#pragma unroll
+                for (int e = 0; e < VEC; e++) reinterpret_cast<T*>(&pack)[e] = acc[v * VEC + e];
+                *reinterpret_cast<V*>(sb + c1_pad<T>(lane * C1_B + v * VEC)) = pack;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int c = lane; c < TILE / VEC; c += 32)
+                *reinterpret_cast<V*>(P.dst + t0 + c * VEC) = *reinterpret_cast<const V*>(sb + c1_pad<T>(c * VEC));
+        } else if (q0 + C1_B <= P.hi) {
 #pragma unroll
             for (int v = 0; v < C1_B / VEC; v++) {
                 V pack;
