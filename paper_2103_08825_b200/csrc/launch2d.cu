@@ -259,13 +259,17 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
         const int* o = &P->offsets[2 * i];
         bp.w[(o[0] + 1) * 3 + (o[1] + 1)] = (T)P->weights[i];
     }
-    // band: side stream, concurrent with the two passes (disjoint outputs)
-    SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
-    SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
-    sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
-                                P->side_stream>>>(bp);
-    SB_CUDA(cudaGetLastError());
-    SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+    // band: side stream, concurrent with the two passes (disjoint outputs), or
+    // (SB200_SEP2D_BAND=1) after them on the main stream
+    static const int band_mode = (int)env_double("SB200_SEP2D_BAND", 0);
+    if (band_mode == 0) {
+        SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
+        SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
+        sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
+                                    P->side_stream>>>(bp);
+        SB_CUDA(cudaGetLastError());
+        SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
+    }
     // staged vertical pass at K = 32 (C3a 2492 -> 2778); at K = 16 the direct one
     // measured faster (1881 vs 1449)
     static const int vsmem = (int)env_double("SB200_SEP2D_VSMEM", 1);
@@ -290,7 +294,13 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     dim3 hg((unsigned)((tiles + sb::SEP_HW - 1) / sb::SEP_HW), (unsigned)(ny - 2 * K));
     sb::sep_hpass_kernel<T, K><<<hg, sb::SEP_HW * 32, 0, P->stream>>>(hp);
     SB_CUDA(cudaGetLastError());
-    SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
+    if (band_mode == 0) {
+        SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
+    } else {
+        sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
+                                    P->stream>>>(bp);
+        SB_CUDA(cudaGetLastError());
+    }
     P->kernels_launched += 2;   // + the vertical pass counted by launch_one
     P->last_kernel = "sep2d (vertical + horizontal composed passes)";
     return SB_OK;

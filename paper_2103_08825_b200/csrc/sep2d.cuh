@@ -233,13 +233,18 @@ __global__ void __launch_bounds__(SEP_BT) sep_band_kernel(const SepBandParams<T>
     const int lx_lo = max(1, -rx0), lx_hi = min(RW - 1, P.nx - rx0);
     // work units: (32-column group, SEG-row segment); a lane walks its column down
     // the segment with a 3 x 3 register window (3 shared loads per cell, not 9)
+    // level l+1 is only needed within K-l-1 cells of the output rectangle (the
+    // cone shrinks by one cell per level): cells farther out are not updated
     constexpr int SEG = 8;
-    const int ncg = (lx_hi - lx_lo + 31) / 32, nseg = (ly_hi - ly_lo + SEG - 1) / SEG;
     for (int l = 0; l < K; l++) {
+        const int sh = l + 1;
+        const int y_lo = max(ly_lo, 1 + sh), y_hi = min(ly_hi, RH - 1 - sh);
+        const int x_lo = max(lx_lo, 1 + sh), x_hi = min(lx_hi, RW - 1 - sh);
+        const int ncg = (x_hi - x_lo + 31) / 32, nseg = (y_hi - y_lo + SEG - 1) / SEG;
         for (int u = warp; u < ncg * nseg; u += SEP_BT / 32) {
-            const int lx = lx_lo + (u % ncg) * 32 + lane;
-            const int r0 = ly_lo + (u / ncg) * SEG, r1 = min(ly_hi, r0 + SEG);
-            if (lx < lx_hi) {
+            const int lx = x_lo + (u % ncg) * 32 + lane;
+            const int r0 = y_lo + (u / ncg) * SEG, r1 = min(y_hi, r0 + SEG);
+            if (lx < x_hi) {
                 const T* c = A + (r0 - 1) * RW + lx;
                 T a0 = c[-1], a1 = c[0], a2 = c[1];
                 c += RW;
