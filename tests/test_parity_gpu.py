@@ -567,6 +567,43 @@ def test_fuzz_fma_within_bar(cfg, dims, k, T, halo):
     assert np_oracle.max_rel_error(got, oracle(spec, box, T)) <= FP64_TOL
 
 
+# --- beyond 2^31 elements: 64-bit addressing in every fused path (impulse response)
+
+@pytest.mark.parametrize("cfg,dims,k,dtype", [
+    ("c3b", (46000, 47000), 4, np.float32),    # 2.16e9 points: level-by-level 2D
+    ("c3a", (46000, 47000), 32, np.float32),   # separable composed 2D
+    ("c4", (1290, 1290, 1300), 2, np.float32), # 3D star, level-by-level (fp32)
+    ("c4", (1290, 1290, 1300), 2, np.float64), # composed 3D star + shell (17 GB per buffer)
+    ("c5", (1290, 1290, 1300), 2, np.float32), # 3D box
+    ("c2", ((1 << 31) + 4096,), 32, np.float32),   # composed 1D
+])
+def test_beyond_2_31_elements_impulse(cfg, dims, k, dtype):
+    spec = config_spec(cfg)
+    assert int(np.prod(dims)) > (1 << 31)
+    box = np.zeros(tuple(n + 2 * spec.r for n in dims), dtype=dtype)
+    T = k
+    at = tuple(n - spec.r * T - 5 for n in dims)   # past 2^31 linearly, cone clear of the halo
+    box[tuple(a + spec.r for a in at)] = 1.0
+    got = sweep(spec, box, T, arith="fma", k=k)
+    # the impulse response is T-fold convolution of the weights, centred at `at`
+    offs, ws = canonical(spec)
+    w = 2 * spec.r * T + 1
+    small = np.zeros((w + 2 * spec.r * T + 2,) * spec.d)
+    c = tuple(sz // 2 for sz in small.shape)
+    small[c] = 1.0
+    for _ in range(T):
+        nxt = np.zeros_like(small)
+        for o, wt in zip(offs, ws):
+            nxt += wt * np.roll(small, shift=tuple(-x for x in o), axis=tuple(range(spec.d)))
+        small = nxt
+    win = tuple(slice(a + spec.r - spec.r * T, a + spec.r + spec.r * T + 1) for a in at)
+    want = small[tuple(slice(cc - spec.r * T, cc + spec.r * T + 1) for cc in c)]
+    np.testing.assert_allclose(got[win], want, rtol=1e-5 if dtype == np.float32 else 1e-12,
+                               atol=1e-7 if dtype == np.float32 else 1e-15)
+    got[win] = 0.0
+    assert not got.any()                    # nothing anywhere else
+
+
 FRESH_PROCESS_CHECK = r"""
 import sys, numpy as np
 sys.path[:0] = [%r, %r]
