@@ -2,6 +2,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <climits>
 #include <cmath>
 
 #include "plan.hpp"
@@ -187,19 +188,43 @@ std::vector<long double> conv_power(const long double w[3], int K) {
     return c;
 }
 
-std::vector<sb::BandItem> band_items(int64_t ny, int64_t nx, int K) {
+// Band regions of the output rows [r0, r1): the K rows next to a physical y side
+// (top / bottom bands, all columns) and the K columns next to the x sides for the
+// rest (left / right bands).
+std::vector<sb::BandItem> band_items(const sb_plan* P, int64_t r0, int64_t r1, int K) {
+    const int64_t ny = P->dims[0], nx = P->dims[1];
     std::vector<sb::BandItem> out;
     const int W = sb::SEP_BW;
-    for (int64_t x = 0; x < nx; x += W) {                  // top / bottom bands: K rows, all columns
-        const int w = (int)std::min<int64_t>(W, nx - x);
-        out.push_back({0, (int32_t)x, K, w});
-        out.push_back({(int32_t)(ny - K), (int32_t)x, K, w});
+    auto rows = [&](int64_t a, int64_t b, bool full) {     // [a, b) intersected with [r0, r1)
+        a = std::max(a, r0);
+        b = std::min(b, r1);
+        if (b <= a) return;
+        if (full) {
+            for (int64_t x = 0; x < nx; x += W)
+                for (int64_t y = a; y < b; y += K)
+                    out.push_back({(int32_t)y, (int32_t)x, (int32_t)std::min<int64_t>(K, b - y),
+                                   (int32_t)std::min<int64_t>(W, nx - x)});
+        } else {
+            for (int64_t y = a; y < b; y += W) {
+                const int h = (int)std::min<int64_t>(W, b - y);
+                out.push_back({(int32_t)y, 0, h, K});
+                out.push_back({(int32_t)y, (int32_t)(nx - K), h, K});
+            }
+        }
+    };
+    const int64_t ylo = P->phys_lo ? K : 0, yhi = P->phys_hi ? ny - K : ny;
+    if (P->phys_lo && P->phys_hi && r0 == 0 && r1 == ny) {
+        // whole grid: top and bottom chunks interleaved per column block
+        for (int64_t x = 0; x < nx; x += W) {
+            const int w = (int)std::min<int64_t>(W, nx - x);
+            out.push_back({0, (int32_t)x, K, w});
+            out.push_back({(int32_t)(ny - K), (int32_t)x, K, w});
+        }
+    } else {
+        if (P->phys_lo) rows(0, K, true);
+        if (P->phys_hi) rows(ny - K, ny, true);
     }
-    for (int64_t y = K; y < ny - K; y += W) {              // left / right bands: K columns
-        const int h = (int)std::min<int64_t>(W, ny - K - y);
-        out.push_back({(int32_t)y, 0, h, K});
-        out.push_back({(int32_t)y, (int32_t)(nx - K), h, K});
-    }
+    rows(ylo, yhi, false);
     return out;
 }
 
@@ -221,7 +246,16 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     vp.sy = P->g.sy;
     vp.nx = (int)nx;
     vp.ny = (int)ny;
+    // pass rows: K from a physical side, the whole slab on a ghost side (the ghost
+    // planes hold the neighbour's rows, depth >= K); intersected with the range
+    const int64_t ylo = std::max<int64_t>(P->phys_lo ? K : 0, range_lo(P));
+    const int64_t yhi = std::min<int64_t>(P->phys_hi ? ny - K : ny, range_hi(P));
+    vp.y0 = (int)ylo;
+    vp.y1 = (int)std::max(ylo, yhi);
+    vp.row_hi = (int)(ny + P->hhi);
     hp = vp;
+    // whole grid (both sides physical, no range): the kernels' fixed-bound form
+    const bool wg = P->phys_lo && P->phys_hi && P->zr_hi < 0;
     const long double la[3] = {a[0], a[1], a[2]}, lb[3] = {b[0], b[1], b[2]};
     const auto ca = conv_power(la, K), cb = conv_power(lb, K);
     for (int i = 0; i < 2 * K + 1; i++) {
@@ -230,19 +264,23 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     }
     // band regions (cached per plan and depth; key -4000 - K)
     Sched1D* sc = nullptr;
+    const int64_t rlo = range_lo(P), rhi = range_hi(P);
     for (auto& e : P->sched1d)
-        if (e.K == -4000 - K) sc = &e;
+        if (e.K == -4000 - K && e.comp_lo == rlo && e.comp_hi == rhi) sc = &e;
     if (!sc) {
-        auto items = band_items(ny, nx, K);
+        auto items = band_items(P, rlo, rhi, K);
         Sched1D e;
         e.K = -4000 - K;
+        e.comp_lo = rlo;
+        e.comp_hi = rhi;
         e.nchunks = (int)items.size();
         SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::BandItem) * items.size()));
         SB_CUDA(cudaMemcpyAsync(e.d_chunks, items.data(), sizeof(sb::BandItem) * items.size(),
                                 cudaMemcpyHostToDevice, P->stream));
         SB_CUDA(cudaStreamSynchronize(P->stream));
         const int smem = sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW);
-        SB_CUDA(cudaFuncSetAttribute(sb::sep_band_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SB_CUDA(cudaFuncSetAttribute(sb::sep_band_kernel<T, K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        SB_CUDA(cudaFuncSetAttribute(sb::sep_band_kernel<T, K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }
@@ -252,6 +290,10 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     bp.sy = P->g.sy;
     bp.nx = (int)nx;
     bp.ny = (int)ny;
+    bp.row_lo = (int)-P->hlo;
+    bp.row_hi = (int)(ny + P->hhi);
+    bp.fix_lo = P->phys_lo ? -1 : INT_MIN / 2;
+    bp.fix_hi = P->phys_hi ? (int)ny : INT_MAX / 2;
     bp.items = reinterpret_cast<const sb::BandItem*>(sc->d_chunks);
     bp.nitems = sc->nchunks;
     for (int i = 0; i < 9; i++) bp.w[i] = T(0);
@@ -262,43 +304,66 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     // band: side stream, concurrent with the two passes (disjoint outputs), or
     // (SB200_SEP2D_BAND=1) after them on the main stream
     static const int band_mode = (int)env_double("SB200_SEP2D_BAND", 0);
-    if (band_mode == 0) {
+    if (band_mode == 0 && sc->nchunks > 0) {
         SB_CUDA(cudaEventRecord(P->fork_ev, P->stream));
         SB_CUDA(cudaStreamWaitEvent(P->side_stream, P->fork_ev, 0));
-        sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
-                                    P->side_stream>>>(bp);
+        const unsigned nb = (unsigned)sc->nchunks;
+        const int bsm = sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW);
+        if (wg)
+            sb::sep_band_kernel<T, K, true><<<nb, sb::SEP_BT, bsm, P->side_stream>>>(bp);
+        else
+            sb::sep_band_kernel<T, K, false><<<nb, sb::SEP_BT, bsm, P->side_stream>>>(bp);
         SB_CUDA(cudaGetLastError());
         SB_CUDA(cudaEventRecord(P->join_ev, P->side_stream));
     }
     // staged vertical pass at K = 32 (C3a 2492 -> 2778); at K = 16 the direct one
     // measured faster (1881 vs 1449)
     static const int vsmem = (int)env_double("SB200_SEP2D_VSMEM", 1);
-    if (vsmem && K == 32) {
+    if (vp.y1 <= vp.y0) {
+        // no pass rows in this range (band rows only)
+    } else if (vsmem && K == 32) {
         constexpr int OUT = sb::SEP_VW * sb::SEP_VB;
         const int smem = sb::sep_vpass_smem_bytes<T, K>();
         static bool attr = false;
         if (!attr) {
-            SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem));
+            SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K, false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             attr = true;
         }
-        dim3 vg((unsigned)((nx + 31) / 32), (unsigned)((ny - 2 * K + OUT - 1) / OUT));
-        sb::sep_vpass_smem_kernel<T, K><<<vg, sb::SEP_VW * 32, smem, P->stream>>>(vp);
+        dim3 vg((unsigned)((nx + 31) / 32), (unsigned)((vp.y1 - vp.y0 + OUT - 1) / OUT));
+        if (wg)
+            sb::sep_vpass_smem_kernel<T, K, true><<<vg, sb::SEP_VW * 32, smem, P->stream>>>(vp);
+        else
+            sb::sep_vpass_smem_kernel<T, K, false><<<vg, sb::SEP_VW * 32, smem, P->stream>>>(vp);
     } else {
-        dim3 vg((unsigned)((nx + sb::SEP_VT - 1) / sb::SEP_VT), (unsigned)((ny - 2 * K + sb::SEP_VB - 1) / sb::SEP_VB));
-        sb::sep_vpass_kernel<T, K><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
+        dim3 vg((unsigned)((nx + sb::SEP_VT - 1) / sb::SEP_VT), (unsigned)((vp.y1 - vp.y0 + sb::SEP_VB - 1) / sb::SEP_VB));
+        if (wg)
+            sb::sep_vpass_kernel<T, K, true><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
+        else
+            sb::sep_vpass_kernel<T, K, false><<<vg, sb::SEP_VT, 0, P->stream>>>(vp);
     }
     SB_CUDA(cudaGetLastError());
     constexpr int TILE = 32 * sb::SEP_HB;
     const int64_t tiles = (nx - 2 * K + TILE - 1) / TILE;
-    dim3 hg((unsigned)((tiles + sb::SEP_HW - 1) / sb::SEP_HW), (unsigned)(ny - 2 * K));
-    sb::sep_hpass_kernel<T, K><<<hg, sb::SEP_HW * 32, 0, P->stream>>>(hp);
-    SB_CUDA(cudaGetLastError());
+    if (vp.y1 > vp.y0) {
+        dim3 hg((unsigned)((tiles + sb::SEP_HW - 1) / sb::SEP_HW), (unsigned)(vp.y1 - vp.y0));
+        if (wg)
+            sb::sep_hpass_kernel<T, K, true><<<hg, sb::SEP_HW * 32, 0, P->stream>>>(hp);
+        else
+            sb::sep_hpass_kernel<T, K, false><<<hg, sb::SEP_HW * 32, 0, P->stream>>>(hp);
+        SB_CUDA(cudaGetLastError());
+    }
     if (band_mode == 0) {
-        SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
-    } else {
-        sb::sep_band_kernel<T, K><<<(unsigned)sc->nchunks, sb::SEP_BT, sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW),
-                                    P->stream>>>(bp);
+        if (sc->nchunks > 0) SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));
+    } else if (sc->nchunks > 0) {
+        const unsigned nb = (unsigned)sc->nchunks;
+        const int bsm = sb::sep_band_smem_bytes<T, K>(K, sb::SEP_BW);
+        if (wg)
+            sb::sep_band_kernel<T, K, true><<<nb, sb::SEP_BT, bsm, P->stream>>>(bp);
+        else
+            sb::sep_band_kernel<T, K, false><<<nb, sb::SEP_BT, bsm, P->stream>>>(bp);
         SB_CUDA(cudaGetLastError());
     }
     P->kernels_launched += 2;   // + the vertical pass counted by launch_one
@@ -317,8 +382,9 @@ int launch_sep2d(sb_plan* P, int src_idx, int k) {
 bool sep2d_ok(const sb_plan* P, int k) {
     static const int enabled = (int)env_double("SB200_SEP2D", 1);
     double a[3], b[3];
-    return enabled && (k == 16 || k == 32) && P->d == 2 && P->phys_lo && P->phys_hi && P->zr_hi < 0 &&
-           P->dims[0] > 2 * k && P->dims[1] > 2 * k && separable_weights(P, a, b);
+    // slab sides need a ghost depth >= k (one launch reads k neighbour rows)
+    return enabled && (k == 16 || k == 32) && P->d == 2 && (P->phys_lo || P->hlo >= k) &&
+           (P->phys_hi || P->hhi >= k) && P->dims[0] > 2 * k && P->dims[1] > 2 * k && separable_weights(P, a, b);
 }
 
 int launch_fused2d(sb_plan* P, int src_idx, int k) {

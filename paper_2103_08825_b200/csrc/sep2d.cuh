@@ -47,14 +47,19 @@ struct SepParams {
     int64_t sy;          // row pitch (elements)
     int nx, ny;
     T c[65];             // composed 1D weights (2K+1), offset -K..K (vertical: a^{*K}; horizontal: b^{*K})
+    int y0, y1;          // output rows [y0, y1) of the passes (K from a physical side)
+    int row_hi;          // rows < row_hi are allocated (input guard of the staged pass)
 };
 
 // tmp[y][x] = sum_m a^{*K}[m] src[y+m][x], rows y in [K, ny-K), all columns.
-template <typename T, int K>
+// WG (whole grid, both y sides physical): the pass rows are [K, ny - K) as
+// compile-time expressions; otherwise [P.y0, P.y1) (slab ghosts / ranges).
+template <typename T, int K, bool WG>
 __global__ void __launch_bounds__(SEP_VT) sep_vpass_kernel(const SepParams<T> P) {
+    const int Y0 = WG ? K : P.y0, Y1 = WG ? P.ny - K : P.y1;
     const int x = blockIdx.x * SEP_VT + threadIdx.x;
-    const int y0 = K + blockIdx.y * SEP_VB;
-    if (x >= P.nx || y0 >= P.ny - K) return;
+    const int y0 = Y0 + blockIdx.y * SEP_VB;
+    if (x >= P.nx || y0 >= Y1) return;
     const T* s = P.src + (int64_t)(y0 - K) * P.sy + x;
     T acc[SEP_VB];
 #pragma unroll
@@ -69,7 +74,7 @@ __global__ void __launch_bounds__(SEP_VT) sep_vpass_kernel(const SepParams<T> P)
     T* d = P.tmp + (int64_t)y0 * P.sy + x;
 #pragma unroll
     for (int o = 0; o < SEP_VB; o++)
-        if (y0 + o < P.ny - K) d[(int64_t)o * P.sy] = acc[o];
+        if (y0 + o < Y1) d[(int64_t)o * P.sy] = acc[o];
 }
 
 // Shared-memory staged form of the vertical pass: a CTA of SEP_VW warps owns 32
@@ -80,18 +85,19 @@ constexpr int SEP_VW = 8;
 template <typename T, int K>
 constexpr int sep_vpass_smem_bytes() { return (2 * K + SEP_VW * SEP_VB) * 32 * (int)sizeof(T); }
 
-template <typename T, int K>
+template <typename T, int K, bool WG>
 __global__ void __launch_bounds__(SEP_VW * 32) sep_vpass_smem_kernel(const SepParams<T> P) {
     extern __shared__ __align__(16) unsigned char smem_v[];
     T* col = reinterpret_cast<T*>(smem_v);            // [row][32]
     constexpr int ROWS = 2 * K + SEP_VW * SEP_VB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x = blockIdx.x * 32 + lane;
-    const int yb = K + blockIdx.y * (SEP_VW * SEP_VB);  // first output row of the CTA
-    const int y_end = P.ny - K;
+    const int yb = (WG ? K : P.y0) + blockIdx.y * (SEP_VW * SEP_VB);  // first output row of the CTA
+    const int y_end = WG ? P.ny - K : P.y1;
+    const int row_hi = WG ? P.ny + 1 : P.row_hi;
     for (int r = warp; r < ROWS; r += SEP_VW) {
-        const int y = yb - K + r;                       // input row (<= ny - 1 + ... guarded)
-        col[r * 32 + lane] = (x < P.nx && y < P.ny + 1) ? P.src[(int64_t)y * P.sy + x] : T(0);
+        const int y = yb - K + r;                       // input row; past the allocation: unused
+        col[r * 32 + lane] = (x < P.nx && y < row_hi) ? P.src[(int64_t)y * P.sy + x] : T(0);
     }
     __syncthreads();
     const int y0 = yb + warp * SEP_VB;
@@ -114,7 +120,7 @@ __global__ void __launch_bounds__(SEP_VW * 32) sep_vpass_smem_kernel(const SepPa
 }
 
 // dst[y][x] = sum_m b^{*K}[m] tmp[y][x+m], rows [K, ny-K), columns [K, nx-K).
-template <typename T, int K>
+template <typename T, int K, bool WG>
 __global__ void __launch_bounds__(SEP_HW * 32) sep_hpass_kernel(const SepParams<T> P) {
     constexpr int VEC = Vec16<T>::n;
     constexpr int TILE = 32 * SEP_HB;
@@ -125,9 +131,9 @@ __global__ void __launch_bounds__(SEP_HW * 32) sep_hpass_kernel(const SepParams<
     static_assert(SPAN % VEC == 0 && (SEP_HB + TAPS - 1) % VEC == 0, "tile span must be 16 B aligned");
     __shared__ __align__(16) T sm[SEP_HW][PADDED];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int y = K + blockIdx.y;
+    const int y = (WG ? K : P.y0) + blockIdx.y;
     const int x0 = K + (blockIdx.x * SEP_HW + warp) * TILE;     // first output of the tile
-    if (x0 >= P.nx - K) return;                                  // (warp-uniform)
+    if (x0 >= P.nx - K || (!WG && y >= P.y1)) return;           // (warp-uniform)
     const T* row = P.tmp + (int64_t)y * P.sy;
     T* buf = sm[warp];
     // inputs x0-K .. x0+TILE+K; columns past nx-1 are never used by a stored output
@@ -200,6 +206,8 @@ struct SepBandParams {
     T* dst;
     int64_t sy;
     int nx, ny;
+    int row_lo, row_hi;  // allocated rows [row_lo, row_hi) (halo or ghost planes included)
+    int fix_lo, fix_hi;  // physical halo rows held fixed (-1 / ny), or out of range on ghost sides
     const BandItem* items;
     int nitems;
     T w[9];              // box weights w[(dy+1)*3 + dx+1]
@@ -210,8 +218,11 @@ struct SepBandParams {
 // outside the allocation are 0, the region's own outer ring (not physical) is
 // never updated -- its staleness spreads one cell per level, K levels never
 // reach the outputs (K+1 away).  Canonical (dy, dx) FMA order per point.
-template <typename T, int K>
+template <typename T, int K, bool WG>
 __global__ void __launch_bounds__(SEP_BT) sep_band_kernel(const SepBandParams<T> P) {
+    // WG: rows -1 and ny are the physical halo (allocated, held fixed)
+    const int row_lo = WG ? -1 : P.row_lo, row_hi = WG ? P.ny + 1 : P.row_hi;
+    const int fix_lo = WG ? -1 : P.fix_lo, fix_hi = WG ? P.ny : P.fix_hi;
     extern __shared__ __align__(16) unsigned char smem_band[];
     T* A = reinterpret_cast<T*>(smem_band);
     const BandItem it = P.items[blockIdx.x];
@@ -221,7 +232,7 @@ __global__ void __launch_bounds__(SEP_BT) sep_band_kernel(const SepBandParams<T>
     // load: allocation = interior plus the 1-cell halo ring
     for (int i = threadIdx.x; i < RH * RW; i += SEP_BT) {
         const int y = ry0 + i / RW, x = rx0 + i % RW;
-        const bool alloc = y >= -1 && y <= P.ny && x >= -1 && x <= P.nx;
+        const bool alloc = y >= row_lo && y < row_hi && x >= -1 && x <= P.nx;
         const T v = alloc ? P.src[(int64_t)y * P.sy + x] : T(0);
         A[i] = v;
         B[i] = v;
@@ -229,7 +240,9 @@ __global__ void __launch_bounds__(SEP_BT) sep_band_kernel(const SepBandParams<T>
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // updatable cells: inside the interior and not on the region's outer ring
-    const int ly_lo = max(1, -ry0), ly_hi = min(RH - 1, P.ny - ry0);
+    // rows: allocated and not a held physical halo row (ghost rows update like interior)
+    const int ly_lo = max(1, max(row_lo, fix_lo + 1) - ry0);
+    const int ly_hi = min(RH - 1, min(row_hi, fix_hi) - ry0);
     const int lx_lo = max(1, -rx0), lx_hi = min(RW - 1, P.nx - rx0);
     // work units: (32-column group, SEG-row segment); a lane walks its column down
     // the segment with a 3 x 3 register window (3 shared loads per cell, not 9)

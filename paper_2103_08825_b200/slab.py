@@ -32,7 +32,8 @@ from .core import GridError, validate
 
 # fused depths the slab plans accept per launch (see sb200.cu fused_k_ok;
 # 1D depths 32 and 64 exist only on the composed path: FMA mode, r*k <= 64)
-_FUSED_KS = {1: (1, 2, 4, 8, 16, 32, 64), 2: (1, 2, 4, 8), 3: (1, 2, 3, 4)}
+# 2D depths 16 and 32 exist only on the separable composed path (FMA mode, rank-1 weights)
+_FUSED_KS = {1: (1, 2, 4, 8, 16, 32, 64), 2: (1, 2, 4, 8, 16, 32), 3: (1, 2, 3, 4)}
 
 
 def split_extent(n: int, world: int) -> list[tuple[int, int]]:

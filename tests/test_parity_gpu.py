@@ -306,7 +306,8 @@ def test_nonfinite_propagation_matches_oracle(cfg, dims, k, arith):
 # --- range launches (slab edge planes first, interior later: sb_launch_range)
 
 @pytest.mark.parametrize("cfg,dims,k,arith", [
-    ("c3b", (60, 130), 4, "exact"), ("c3a", (61, 140), 8, "fma"), ("c4", (30, 37, 70), 2, "fma"),
+    ("c3b", (60, 130), 4, "exact"), ("c3a", (61, 140), 8, "fma"), ("c3a", (130, 150), 32, "fma"),
+    ("c3a", (90, 150), 16, "fma"), ("c4", (30, 37, 70), 2, "fma"),
     ("c4", (30, 37, 70), 3, "exact"), ("c5", (25, 33, 66), 2, "fma"), ("p:2d5p", (33, 50), 1, "exact"),
 ])
 def test_range_launches_compose_a_full_launch(cfg, dims, k, arith):

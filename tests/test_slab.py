@@ -137,6 +137,26 @@ def test_single_gpu_slab_emulation_bit_identical(cfg, dims, k, g):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("k,g", [(32, 2), (16, 3)])
+def test_single_gpu_slab_emulation_sep2d_matches_whole_grid(k, g):
+    # separable composed 2D (FMA, rank-1 weights): row slabs with k-deep ghosts
+    # reproduce the whole-grid plan bit for bit (same composed weights per row,
+    # x bands on each slab, y bands on the physical sides only); exchange overlapped
+    spec = config_spec("c3a")
+    dims = (300, 333)
+    gbox = seeded_box(dims, 1, seed=8)
+    sweeps = [SlabSweep(spec, dims, rank=r, world=g, k=k, arith="fma", device=0) for r in range(g)]
+    for s in sweeps:
+        s.upload(s.local_box(gbox))
+    steps = 2 * k
+    run_local(sweeps, steps)
+    got = np.concatenate([s.download()[s.geom.interior_slice()] for s in sweeps], axis=0)
+    from paper_2103_08825_b200.plan import sweep
+    whole = sweep(spec, gbox, steps, arith="fma", k=k)
+    assert got.tobytes() == whole[1:1 + dims[0]].tobytes()
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("g", [2, 3])
 def test_single_gpu_slab_emulation_composed3d_matches_whole_grid(g):
     # composed 3D star (FMA, k=2): z-slabs with 2-plane ghosts reproduce the
