@@ -48,7 +48,7 @@ WORKLOADS = {
     "c1": dict(spec="c1", dims=(1 << 20,), T=64, name="1D3P fp64 N=2^20 T=64"),
     "c2": dict(spec="c2", dims=(1 << 26,), T=1000, name="1D5P fp64 N=2^26 T=1000"),
     # slab_k: the fused depth of the slab plans at N > 1 (N = 1 takes the plan default)
-    "c3a": dict(spec="c3a", dims=(16384, 16384), T=500, slab_k=4, name="2D9P fp64 16384^2 T=500 (weights 1/9)"),
+    "c3a": dict(spec="c3a", dims=(16384, 16384), T=500, slab_k=32, name="2D9P fp64 16384^2 T=500 (weights 1/9)"),
     "c3b": dict(spec="c3b", dims=(16384, 16384), T=500, slab_k=4, name="2D9P fp64 16384^2 T=500 (seeded random weights)"),
     "c4": dict(spec="c4", dims=(512, 512, 512), T=200, slab_k=2, name="3D7P fp64 512^3 T=200"),
     "c5": dict(spec="c5", dims=(768, 768, 768), T=100, slab_k=2, name="3D27P fp64 768^3 T=100"),
