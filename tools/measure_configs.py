@@ -14,14 +14,13 @@ import argparse
 import json
 import os
 import sys
-import time
 
 import numpy as np
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
-from paper_2103_08825_b200.core import CONFIGS, canonical, config_spec  # noqa: E402
+from paper_2103_08825_b200.core import CONFIGS, config_spec  # noqa: E402
 from paper_2103_08825_b200.plan import Plan  # noqa: E402
 
 KS = {1: (1, 2, 4, 8, 16, 32, 64), 2: (1, 2, 4, 8, 16, 32), 3: (1, 2, 3, 4)}
@@ -92,18 +91,12 @@ def main():
             entry["best_gstencil"] = best[1]["gstencil"]
             entry["best_frac"] = best[1]["frac"]
             if not args.no_cpu:
-                from oracle import c_oracle
-                offs, ws = canonical(spec)
-                cb = np.array(box, copy=True)
-                t0 = time.perf_counter()
-                c_oracle.sweep(cb, spec.r, offs, ws, 1, inplace=True)
-                one = time.perf_counter() - t0
-                steps = int(max(1, min(T, 8.0 / max(one, 1e-6))))
-                t0 = time.perf_counter()
-                c_oracle.sweep(cb, spec.r, offs, ws, steps, inplace=True)
-                dt_cpu = time.perf_counter() - t0
-                entry["cpu_oracle"] = {"gstencil": round(n * steps / dt_cpu / 1e9, 4), "steps_sampled": steps,
-                                       "threads": c_oracle.max_threads(), "dtype": "f64"}
+                # bench.py's cpu_baseline leg (the oracle port on all host threads, ~8 s sample)
+                from bench import cpu_reference_rate
+                rate, threads, sample = cpu_reference_rate(spec, dims, budget_s=8.0)
+                entry["cpu_oracle"] = {"gstencil": round(rate, 4), "sample": sample,
+                                       "threads": threads, "dtype": "f64",
+                                       "source": "bench.cpu_reference_rate (the cpu_baseline leg)"}
                 entry["speedup_vs_cpu_oracle"] = round(entry["best_gstencil"] / entry["cpu_oracle"]["gstencil"], 1)
             results[f"{key}_{dt}"] = entry
             print(key, dt, {k: (v["gstencil"], v["frac"]) for k, v in entry["k"].items()},
