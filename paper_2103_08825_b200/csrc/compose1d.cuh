@@ -185,11 +185,17 @@ compose1d_kernel(const Compose1DParams<T> P, const EdgeWindowParams<T, (R > 0 ? 
         cp_async_wait<1>();
         __syncwarp();
         const T* s = buf + cur * PADDED;
+        // lane window base; with C1_B/VEC a multiple of 4 chunks the padding of
+        // lane * C1_B + jj splits into a lane part and a compile-time jj part,
+        // so every window load is the base plus an immediate offset
+        constexpr bool SPLIT = (C1_B / VEC) % 4 == 0;
+        const T* sl = s + (SPLIT ? c1_pad<T>(lane * C1_B) : 0);
         T acc[C1_B];
         using V = typename Vec16<T>::type;
 #pragma unroll
         for (int jj = 0; jj < C1_B + TAPS - 1; jj += VEC) {
-            const V xv = *reinterpret_cast<const V*>(s + c1_pad<T>(lane * C1_B + jj));   // 16 B, conflict-free
+            const int off = SPLIT ? jj + (jj / (4 * VEC)) * VEC : c1_pad<T>(lane * C1_B + jj);
+            const V xv = *reinterpret_cast<const V*>(sl + off);   // 16 B, conflict-free
 #pragma unroll
             for (int e = 0; e < VEC; e++) {
                 const int j = jj + e;

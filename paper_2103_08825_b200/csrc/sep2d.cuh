@@ -153,9 +153,14 @@ __global__ void __launch_bounds__(SEP_HW * 32) sep_hpass_kernel(const SepParams<
     __syncwarp();
     T acc[SEP_HB];
     using V = typename Vec16<T>::type;
+    // lane window base + compile-time offsets when SEP_HB/VEC is a multiple of 4
+    // chunks (see compose1d_kernel)
+    constexpr bool SPLIT = (SEP_HB / VEC) % 4 == 0;
+    const T* bl = buf + (SPLIT ? c1_pad<T>(lane * SEP_HB) : 0);
 #pragma unroll
     for (int jj = 0; jj < SEP_HB + TAPS - 1; jj += VEC) {
-        const V xv = *reinterpret_cast<const V*>(buf + c1_pad<T>(lane * SEP_HB + jj));
+        const int off = SPLIT ? jj + (jj / (4 * VEC)) * VEC : c1_pad<T>(lane * SEP_HB + jj);
+        const V xv = *reinterpret_cast<const V*>(bl + off);
 #pragma unroll
         for (int e = 0; e < VEC; e++) {
             const int j = jj + e;
