@@ -26,7 +26,10 @@ namespace sb {
 #ifndef SB_C1_COALESCED_STORES
 #define SB_C1_COALESCED_STORES 1
 #endif
-constexpr int C1_B = 8;          // outputs per lane per tile
+#ifndef SB_C1_B
+#define SB_C1_B 8
+#endif
+constexpr int C1_B = SB_C1_B;     // outputs per lane per tile
 constexpr int C1_WARPS = 4;
 constexpr int C1_MAXTAPS = 129;  // R*K <= 64
 
