@@ -78,8 +78,11 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
 
     ``ranges`` = [(lo, hi)] per axis restricts the step to that interior
     sub-box, as the reference's tiled runner drives it (tiling.py:353-354):
-    the device computes only the box (sb_step_box) and only the box of
-    ``dst`` is written; counters count the box's points (kernels.py:127-134).
+    the device computes only the box and only the box of ``dst`` is written;
+    counters count the box's points (kernels.py:127-134).  NATURAL grids move
+    only the box plus its r-deep neighbourhood host<->device; BLOCK_TRANSPOSE
+    / DLT grids are un-permuted whole on the device and stepped with
+    sb_step_box.
     Grids may be NATURAL, BLOCK_TRANSPOSE or DLT (both in the same layout).
     """
     _check_pair(src, dst)
@@ -90,6 +93,20 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
         ranges = _check_ranges(ranges, src.dims)
         if any(hi <= lo for lo, hi in ranges):
             return                                   # empty box: nothing computed or counted
+    if ranges is not None and natural:
+        # Only the box and its r-deep neighbourhood travel: the box is swept as
+        # a grid of its own whose halo is src's values around it (the cells the
+        # step reads, kernels.py:103-108), so each point sums the same terms in
+        # the same order as in a whole-grid step.
+        sub = compact_view(src)[tuple(slice(lo, hi + 2 * r) for lo, hi in ranges)]
+        with Plan(spec, tuple(hi - lo for lo, hi in ranges), arith=arith, k=1, kernel="generic") as p:
+            p.upload(np.ascontiguousarray(sub, dtype=np.float64))
+            p.run(1)
+            out = p.download()
+        interior_view(dst)[tuple(slice(lo, hi) for lo, hi in ranges)] = \
+            out[tuple(slice(r, s - r) for s in out.shape)]
+        _count(counters, spec, int(np.prod([hi - lo for lo, hi in ranges])))
+        return
     kernel = "generic" if ranges is not None else "auto"
     with Plan(spec, tuple(src.dims), arith=arith, k=1, kernel=kernel) as p:
         if natural:
@@ -110,7 +127,11 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
             interior_view(dst)[sel] = out[sel_box]
     else:
         _store_interior(dst, out, ranges)
-    pts = _points(src) if ranges is None else int(np.prod([hi - lo for lo, hi in ranges]))
+    _count(counters, spec, _points(src) if ranges is None else int(np.prod([hi - lo for lo, hi in ranges])))
+
+
+def _count(counters, spec, pts: int) -> None:
+    """Meter one step over ``pts`` points as scalar_step does (kernels.py:127-134)."""
     if counters is not None:
         counters.point_updates += pts
         counters.scalar_loads += len(spec.weights) * pts

@@ -53,6 +53,9 @@ def _oracle_step(spec, src):
     ("2d5p", (40, 70), [(0, 40), (33, 70)]),
     ("3d27p", (9, 20, 33), [(2, 7), (5, 6), (1, 32)]),
     ("3d7p", (8, 21, 30), [(0, 8), (0, 21), (0, 30)]),
+    ("2d9p", (41, 66), [(40, 41), (65, 66)]),          # one corner point
+    ("1d3p", (64,), [(0, 1)]),
+    ("3d27p", (6, 7, 9), [(0, 1), (3, 7), (8, 9)]),
 ])
 def test_step_ranges_writes_only_the_box(preset, dims, ranges):
     # scalar_step(..., ranges=...) semantics (kernels.py:88-134)
