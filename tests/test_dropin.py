@@ -39,6 +39,28 @@ def test_step_rejects_aliasing_and_bad_ranges():
     assert c.point_updates == 0
 
 
+@pytest.mark.parametrize("preset,dims,ranges", [
+    ("1d5p", (1000,), [(17, 403)]),
+    ("2d9p", (41, 66), [(40, 41), (65, 66)]),
+    ("3d27p", (9, 20, 33), [(2, 7), (5, 6), (1, 32)]),
+    ("3d7p", (6, 7, 9), [(0, 6), (0, 7), (0, 9)]),
+])
+def test_box_as_own_grid_is_the_whole_step_restricted(preset, dims, ranges):
+    # the premise of b200_step's NATURAL ranges path, checked on the oracle:
+    # stepping the box + r neighbourhood as a grid of its own (its halo = src
+    # around the box) gives bit for bit the whole-grid step on the box
+    spec = make_stencil_spec(preset)
+    src = alloc_grid(spec, dims)
+    src.set_interior(np.random.default_rng(11).random(dims))
+    offs, ws = canonical(spec)
+    r = spec.r
+    box = compact_view(src)[tuple(slice(lo, hi + 2 * r) for lo, hi in ranges)]
+    got = c_oracle.sweep(np.ascontiguousarray(box), r, offs, ws, 1)
+    got = got[tuple(slice(r, s - r) for s in got.shape)]
+    want = _oracle_step(spec, src)[tuple(slice(lo, hi) for lo, hi in ranges)]
+    assert np.array_equal(got, want)
+
+
 def _oracle_step(spec, src):
     offs, ws = canonical(spec)
     want = c_oracle.sweep(np.ascontiguousarray(compact_view(src)), spec.r, offs, ws, 1)
