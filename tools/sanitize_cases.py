@@ -1,4 +1,5 @@
-"""Small fused 1D/2D/3D sweeps incl. slab (ghost) plans, for compute-sanitizer memcheck."""
+"""Small fused 1D/2D/3D sweeps incl. slab (ghost) plans, composed paths and ranges steps, for
+compute-sanitizer memcheck (closed on the current GPU pool: run plainly there as an exit-0 smoke)."""
 import os
 import sys
 
@@ -53,4 +54,25 @@ for cfg, dims, lay, vl in (("c1", (70,), "block_transpose", 4), ("c2", (203,), "
     (tr.to_block_transpose if lay == "block_transpose" else tr.to_dlt)(g, vl)
     b200_sweep(g, spec, 2, 3)
     (tr.from_block_transpose if lay == "block_transpose" else tr.from_dlt)(g)
+# composed 1D (FMA, k=32/64, boundary windows in the launch) and separable composed 2D (c3a, k=16/32)
+for cfg, dims, ks in (("c2", (20000,), (32,)), ("c1", (13001,), (64,)), ("c3a", (70, 300), (16, 32)),
+                      ("c3a", (131, 97), (32,))):
+    spec = config_spec(cfg)
+    box = rng.random(tuple(n + 2 * spec.r for n in dims))
+    for k in ks:
+        sweep(spec, box, 2 * k + 3, k=k, arith="fma")
+spec = config_spec("c3a")
+sw = [SlabSweep(spec, (140, 300), rank=r, world=2, k=32, arith="fma") for r in range(2)]
+gbox = rng.random((142, 302))
+for s in sw:
+    s.upload(s.local_box(gbox))
+run_local(sw, 64)
+# ranges-restricted steps (box swept as its own grid; BLOCK_TRANSPOSE via sb_step_box)
+from paper_2103_08825_b200.kernels import b200_step  # noqa: E402
+from paper_2103_08825_b200.grid import alloc_like  # noqa: E402
+for cfg, dims, rg in (("c5", (9, 20, 33), [(2, 7), (5, 6), (1, 32)]), ("c3b", (41, 66), [(40, 41), (0, 66)])):
+    spec = config_spec(cfg)
+    g = alloc_grid(spec, dims)
+    g.set_interior(rng.random(dims))
+    b200_step(g, alloc_like(g), spec, ranges=rg)
 print("sanitize cases done")
