@@ -95,7 +95,7 @@ typedef struct sb_problem {
 
 typedef struct sb_timing {
     double device_ms;        /* CUDA-event time of the whole call on the plan stream */
-    double kernel_ms;        /* CUDA-event time of the main kernel launches only */
+    double kernel_ms;        /* equal to device_ms: sb_run enqueues kernels only (no copies) */
     int64_t launches;        /* kernels launched by the call */
     int64_t point_updates;   /* interior points x steps (Counters.point_updates) */
     int32_t k_used;          /* fused steps per main launch */

@@ -1,3 +1,4 @@
+#include <atomic>
 // Launch unit of the fused 1D kernel (K1): guided chunk schedule, edge-kernel fork/join.
 #include <cstdio>
 #include <cstdlib>
@@ -214,11 +215,11 @@ int launch_compose1d_k(sb_plan* P, const T* src, T* dst) {
         const int main_blocks = std::max(1, sc->blocks - sc->nedge);
         cp.total_warps = main_blocks * sb::C1_WARPS;
         auto ck = sb::compose1d_kernel<T, HALF, R>;
-        static bool attr_set = false;   // per instantiation
-        if (!attr_set) {
+        static std::atomic<unsigned long long> attr_set{0};   // per instantiation, one bit per device
+        if (!((attr_set.load() >> (P->device & 63)) & 1ull)) {
             SB_CUDA(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          sb::compose1d_smem_bytes<T, HALF>()));
-            attr_set = true;
+            attr_set.fetch_or(1ull << (P->device & 63));
         }
         ck<<<(unsigned)(main_blocks + sc->nedge), sb::C1_WARPS * 32, sb::compose1d_smem_bytes<T, HALF>(), P->stream>>>(
             cp, ep, sc->nedge);

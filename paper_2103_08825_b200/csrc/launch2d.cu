@@ -1,3 +1,4 @@
+#include <atomic>
 // Launch unit of the fused 2D kernel (K2): strip/segment work items.
 #include <cstdio>
 #include <cstdlib>
@@ -70,9 +71,12 @@ bool separable_weights(const sb_plan* P, double a[3], double b[3]) {
         a[i] = w[i][1];
         b[i] = w[1][i] / w[1][1];
     }
+    // exactly rank 1 in double (a near-separable table would run a slightly
+    // different operator whose error grows with T): otherwise the 9-term path
+    (void)wmax;
     for (int i = 0; i < 3; i++)
         for (int j = 0; j < 3; j++)
-            if (std::fabs(a[i] * b[j] - w[i][j]) > 1e-14 * wmax) return false;
+            if (a[i] * b[j] != w[i][j]) return false;
     return true;
 }
 
@@ -324,13 +328,13 @@ int launch_sep2d_k(sb_plan* P, int src_idx) {
     } else if (vsmem && K == 32) {
         constexpr int OUT = sb::SEP_VW * sb::SEP_VB;
         const int smem = sb::sep_vpass_smem_bytes<T, K>();
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<unsigned long long> attr{0};   // one bit per device
+        if (!((attr.load() >> (P->device & 63)) & 1ull)) {
             SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             SB_CUDA(cudaFuncSetAttribute(sb::sep_vpass_smem_kernel<T, K, false>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            attr = true;
+            attr.fetch_or(1ull << (P->device & 63));
         }
         dim3 vg((unsigned)((nx + 31) / 32), (unsigned)((vp.y1 - vp.y0 + OUT - 1) / OUT));
         if (wg)

@@ -550,19 +550,16 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
         lin[i] = o;
     }
     SB_CUDA_P(cudaMalloc(&P->d_counter, 4 * sizeof(unsigned int)));
-    SB_CUDA_P(cudaMemset(P->d_counter, 0, 4 * sizeof(unsigned int)));
+    SB_CUDA_P(cudaMemsetAsync(P->d_counter, 0, 4 * sizeof(unsigned int), P->stream));
     SB_CUDA_P(cudaMalloc(&P->d_lin, sizeof(int64_t) * P->nw));
-    SB_CUDA_P(cudaMemcpy(P->d_lin, lin.data(), sizeof(int64_t) * P->nw, cudaMemcpyHostToDevice));
+    SB_CUDA_P(cudaMemcpyAsync(P->d_lin, lin.data(), sizeof(int64_t) * P->nw, cudaMemcpyHostToDevice, P->stream));
     SB_CUDA_P(cudaMalloc(&P->d_w, P->es * P->nw));
-    if (P->dtype == SB_F64) {
-        SB_CUDA_P(cudaMemcpy(P->d_w, P->weights.data(), 8 * P->nw, cudaMemcpyHostToDevice));
-    } else {
-        std::vector<float> wf(P->weights.begin(), P->weights.end());
-        SB_CUDA_P(cudaMemcpy(P->d_w, wf.data(), 4 * P->nw, cudaMemcpyHostToDevice));
-    }
-    // the setup above mixes the legacy stream (memset/memcpy) and the non-blocking
-    // plan stream: wait for both before any kernel can read these tables
-    SB_CUDA_P(cudaDeviceSynchronize());
+    std::vector<float> wf(P->weights.begin(), P->weights.end());
+    SB_CUDA_P(cudaMemcpyAsync(P->d_w, P->dtype == SB_F64 ? (const void*)P->weights.data() : (const void*)wf.data(),
+                              P->es * P->nw, cudaMemcpyHostToDevice, P->stream));
+    // every setup operation is ordered on the plan stream: wait for that stream
+    // only (no device-wide sync -- plans of concurrent host threads stay independent)
+    SB_CUDA_P(cudaStreamSynchronize(P->stream));
 #undef SB_CUDA_P
     *out = P;
     return SB_OK;

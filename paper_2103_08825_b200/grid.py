@@ -156,14 +156,21 @@ def storage_rows(grid) -> int:
     return int(np.prod(grid.data.shape[:-1])) if grid.data.ndim > 1 else 1
 
 
-def compact_view(grid) -> np.ndarray:
+def compact_view(grid, r: int | None = None) -> np.ndarray:
     """Halo-inclusive compact box view (C-ABI host convention) of a NATURAL grid.
 
-    Outer axes keep their r halo; on the unit axis the r cells adjacent to the
-    interior (the only ones NATURAL sweeps read, kernels.py:89-100).
+    ``r`` is the stencil order of the sweep (default: the order the grid was
+    allocated for).  A grid sized for a larger order than the stencil's is
+    legal in the reference (``_region`` offsets by the grid's own halo,
+    kernels.py:88-100): the view keeps the r cells next to the interior on
+    every axis -- the only ones a NATURAL sweep of order r reads.
     """
-    r, hu = grid.r, grid.halo_unit
-    return grid.data[..., hu - r:hu + grid.unit_n + r]
+    g_r, hu = grid.r, grid.halo_unit
+    r = g_r if r is None else int(r)
+    if r > g_r:
+        raise GridError(f"grid halo sized for order {g_r} cannot serve a stencil of order {r}")
+    outer = tuple(slice(g_r - r, g_r + n + r) for n in grid.dims[:-1])
+    return grid.data[outer + (slice(hu - r, hu + grid.unit_n + r),)]
 
 
 def _outer_interior(grid) -> np.ndarray:

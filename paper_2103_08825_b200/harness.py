@@ -68,8 +68,13 @@ class BenchConfig:
     steps: int
     method: str = "b200"
     vl: int = 4
-    jam_k: int = 8                 # fused steps per HBM round trip (the reference's jam factor)
+    jam_k: int = 0                 # fused steps per HBM round trip (the reference's jam
+                                   # factor); 0 = the plan's default depth for the stencil class
+    block: tuple | None = None     # host tiling (harness.py:47-48): the b200 methods tile on
+    tile_height: int | None = None  # the device, so these must stay None (UsageError)
+    workers: int = 1
     seed: int = 12345
+    csv_path: str | None = None
     verify: bool = False
     weights: object = None         # StencilSpec | BASELINE config key | None (preset `stencil`)
 
@@ -96,7 +101,7 @@ class BenchResult:
         err = "" if self.max_rel_err is None else f"{self.max_rel_err:.17g}"
         return ",".join([
             cfg.stencil, cfg.method, str(cfg.vl), str(cfg.jam_k), "x".join(map(str, cfg.dims)),
-            str(cfg.steps), "", "", "1", f"{self.seconds:.17g}", f"{self.layout_seconds:.17g}",
+            str(cfg.steps), "", "", str(cfg.workers), f"{self.seconds:.17g}", f"{self.layout_seconds:.17g}",
             f"{self.gflops:.17g}", err, str(self.counters.element_loads(cfg.vl)),
             str(self.counters.element_stores(cfg.vl)), str(self.counters.reorg_ops),
         ])
@@ -115,8 +120,13 @@ def validate_config(cfg: BenchConfig) -> None:
         raise UsageError(f"--steps {cfg.steps}: must be >= 1")
     if cfg.vl not in (4, 8):
         raise UsageError(f"--vl {cfg.vl}: supported vector lengths are 4 and 8")
-    if cfg.jam_k < 1:
-        raise UsageError(f"--jam-k {cfg.jam_k}: must be >= 1")
+    if cfg.jam_k < 0:
+        raise UsageError(f"--jam-k {cfg.jam_k}: must be >= 0 (0 = the plan's default depth)")
+    if cfg.block is not None or cfg.tile_height is not None:
+        raise UsageError("--block/--tile-height: the b200 methods tile on the device; for host "
+                         "tessellate tiling register them in the reference's METHODS and use run_tiled")
+    if cfg.workers < 1:
+        raise UsageError(f"--threads {cfg.workers}: must be >= 1")
 
 
 def seed_grid(cfg: BenchConfig, spec: StencilSpec):

@@ -30,7 +30,7 @@ import numpy as np
 
 from .core import GridError, validate
 from .grid import compact_view, interior_view, is_natural, layout_value, unit_permutation
-from .plan import Plan
+from .plan import cached_plan
 
 
 def _check_pair(src, dst) -> None:
@@ -98,26 +98,28 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
         # a grid of its own whose halo is src's values around it (the cells the
         # step reads, kernels.py:103-108), so each point sums the same terms in
         # the same order as in a whole-grid step.
-        sub = compact_view(src)[tuple(slice(lo, hi + 2 * r) for lo, hi in ranges)]
-        with Plan(spec, tuple(hi - lo for lo, hi in ranges), arith=arith, k=1, kernel="generic") as p:
-            p.upload(np.ascontiguousarray(sub, dtype=np.float64))
-            p.run(1)
-            out = p.download()
+        sub = compact_view(src, r)[tuple(slice(lo, hi + 2 * r) for lo, hi in ranges)]
+        p = cached_plan(spec, tuple(hi - lo for lo, hi in ranges), arith=arith, k=1, kernel="generic")
+        p.upload(np.ascontiguousarray(sub, dtype=np.float64))
+        p.run(1)
+        out = p.download()
         interior_view(dst)[tuple(slice(lo, hi) for lo, hi in ranges)] = \
             out[tuple(slice(r, s - r) for s in out.shape)]
         _count(counters, spec, int(np.prod([hi - lo for lo, hi in ranges])))
         return
+    if not natural and src.r != r:
+        raise GridError(f"{layout_value(src)} grid sized for order {src.r}, stencil order {r}")
     kernel = "generic" if ranges is not None else "auto"
-    with Plan(spec, tuple(src.dims), arith=arith, k=1, kernel=kernel) as p:
-        if natural:
-            p.upload(np.ascontiguousarray(compact_view(src), dtype=np.float64))
-        else:
-            p.upload_storage(src)
-        if ranges is not None:
-            p.step_box(ranges)
-        else:
-            p.run(1)
-        out = p.download() if natural else p.download_storage(src)
+    p = cached_plan(spec, tuple(src.dims), arith=arith, k=1, kernel=kernel)
+    if natural:
+        p.upload(np.ascontiguousarray(compact_view(src, r), dtype=np.float64))
+    else:
+        p.upload_storage(src)
+    if ranges is not None:
+        p.step_box(ranges)
+    else:
+        p.run(1)
+    out = p.download() if natural else p.download_storage(src)
     if natural:
         if ranges is None:
             interior_view(dst)[...] = out[tuple(slice(r, s - r) for s in out.shape)]
@@ -150,18 +152,20 @@ def b200_sweep(grid, spec, k, T, counters=None, *, arith="exact") -> None:
     if T < 0:
         raise GridError(f"total steps T={T} must be >= 0")
     natural = is_natural(grid)
-    with Plan(spec, tuple(grid.dims), arith=arith, k=k) as p:
-        if natural:
-            p.upload(np.ascontiguousarray(compact_view(grid), dtype=np.float64))
-        else:
-            p.upload_storage(grid)
-        p.run(T)
-        if natural:
-            out = p.download()
-            interior_view(grid)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
-        else:
-            out = p.download_storage(grid)
-            _store_interior(grid, out)
+    if not natural and grid.r != spec.r:
+        raise GridError(f"{layout_value(grid)} grid sized for order {grid.r}, stencil order {spec.r}")
+    p = cached_plan(spec, tuple(grid.dims), arith=arith, k=k)
+    if natural:
+        p.upload(np.ascontiguousarray(compact_view(grid, spec.r), dtype=np.float64))
+    else:
+        p.upload_storage(grid)
+    p.run(T)
+    if natural:
+        out = p.download()
+        interior_view(grid)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
+    else:
+        out = p.download_storage(grid)
+        _store_interior(grid, out)
     if counters is not None:
         counters.point_updates += _points(grid) * T
 

@@ -9,6 +9,8 @@ compact halo-inclusive box convention of include/sb200.h.
 from __future__ import annotations
 
 import ctypes
+import threading
+from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -231,6 +233,46 @@ def storage_descriptor(grid) -> _abi.SbStorage:
     return st
 
 
+_CACHE = threading.local()
+PLAN_CACHE_SIZE = 8     # plans kept per host thread (device memory stays allocated)
+
+
+def cached_plan(spec, dims, *, dtype="f64", arith="fma", k=0, kernel="auto", device=0) -> "Plan":
+    """A Plan for this problem from the calling thread's LRU cache.
+
+    Repeated single steps / tiles / sweeps of one geometry (the reference's
+    ``_execute`` loop and tile runner call a step function once per time step
+    and tile) reuse the device buffers, streams and schedules instead of
+    allocating them per call.  Plans are per host thread (a plan serves one
+    host thread at a time, include/sb200.h), so concurrent callers -- the
+    reference's ThreadPoolExecutor tile workers -- never share one.
+    """
+    offs, ws = canonical(spec)
+    key = (spec.d, spec.r, spec.shape, tuple(offs), tuple(ws), tuple(int(n) for n in dims),
+           dtype, arith, int(k), kernel, int(device))
+    cache = getattr(_CACHE, "plans", None)
+    if cache is None:
+        cache = _CACHE.plans = OrderedDict()
+    p = cache.get(key)
+    if p is not None and p._h:
+        cache.move_to_end(key)
+        return p
+    p = Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device)
+    cache[key] = p
+    while len(cache) > PLAN_CACHE_SIZE:
+        _, old = cache.popitem(last=False)
+        old.close()
+    return p
+
+
+def clear_plan_cache() -> None:
+    """Release the calling thread's cached plans (their device memory)."""
+    cache = getattr(_CACHE, "plans", None)
+    while cache:
+        _, p = cache.popitem()
+        p.close()
+
+
 def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
           device=0, dtype=None) -> np.ndarray:
     """``steps`` Jacobi steps of ``spec`` over a compact halo-inclusive ``box``.
@@ -254,4 +296,4 @@ def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
         return p.download()
 
 
-__all__ = ["Plan", "Timing", "sweep", "host_shape", "storage_descriptor", "SpecError", "GridError"]
+__all__ = ["Plan", "Timing", "sweep", "cached_plan", "clear_plan_cache", "host_shape", "storage_descriptor", "SpecError", "GridError"]

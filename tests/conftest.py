@@ -19,6 +19,16 @@ if REPO not in sys.path:
 
 GOLDEN_DIR = os.path.join(REPO, "tests", "golden")
 
+# The reference package (stencilbench) for the integration tests: the per-pod
+# install under baseline/_ref (travels to the GPU box with the repo), else the
+# read-only source tree of this build container.  Tests that need it skip
+# when neither exists.
+for _ref in (os.path.join(REPO, "baseline", "_ref"), "/root/reference/pkg/src"):
+    if os.path.isdir(os.path.join(_ref, "stencilbench")):
+        if _ref not in sys.path:
+            sys.path.append(_ref)
+        break
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

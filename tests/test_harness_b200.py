@@ -25,7 +25,8 @@ def oracle_interior(cfg, spec):
 
 @pytest.mark.parametrize("bad,match", [
     (dict(method="scalar"), "unknown"), (dict(dims=(10, 10)), "needs 1 extents"),
-    (dict(steps=0), "steps"), (dict(vl=6), "vl"), (dict(jam_k=0), "jam-k"), (dict(dims=(0,)), "positive"),
+    (dict(steps=0), "steps"), (dict(vl=6), "vl"), (dict(jam_k=-1), "jam-k"), (dict(dims=(0,)), "positive"),
+    (dict(block=(16,), tile_height=4), "device"), (dict(workers=0), "threads"),
 ])
 def test_validate_config_rejects(bad, match):
     kw = dict(stencil="1d3p", dims=(64,), steps=3)
@@ -52,7 +53,16 @@ def test_seed_grid_matches_reference_convention():
 def test_csv_row_field_order():
     res = BenchResult(BenchConfig("1d5p", (100,), 4), 0.5, 0.1, 2.0, Counters(point_updates=400))
     assert len(res.csv_row().split(",")) == len(CSV_HEADER.split(","))
-    assert res.csv_row().startswith("1d5p,b200,4,8,100,4,")
+    assert res.csv_row().startswith("1d5p,b200,4,0,100,4,,,1,")
+
+
+def test_default_depth_is_valid_for_every_stencil_class():
+    # jam_k defaults to 0 = the plan's own depth, so a default BenchConfig is
+    # valid for 3D stencils too (a fixed default of 8 is rejected by the 3D kernels)
+    for stencil, dims in (("1d3p", (64,)), ("2d9p", (8, 8)), ("3d7p", (4, 4, 4)), ("3d27p", (4, 4, 4))):
+        cfg = BenchConfig(stencil, dims, 3)
+        assert cfg.jam_k == 0
+        validate_config(cfg)
 
 
 @pytest.mark.gpu
@@ -66,6 +76,13 @@ def test_run_benchmark_bit_identical_to_oracle(method, stencil, dims, steps, k):
     assert res.max_rel_err == 0.0
     assert res.counters.point_updates == int(np.prod(dims)) * steps
     assert res.gflops > 0 and (res.layout_seconds > 0) == (method != "b200")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stencil,dims", [("3d7p", (9, 10, 40)), ("3d27p", (7, 9, 33)), ("2d9p", (21, 45))])
+def test_run_benchmark_default_depth(stencil, dims):
+    res = run_benchmark(BenchConfig(stencil, dims, 5, verify=True), oracle=oracle_interior)
+    assert res.max_rel_err == 0.0
 
 
 @pytest.mark.gpu
