@@ -1,24 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the multistep stencil sweep (BASELINE.json metric).
 
-Workload (N=1, default): BASELINE configs[1] = C2, 1D 5-point Jacobi fp64,
-N=2^26 interior points, T=1000 steps, coefficients (1/16, 1/4, 3/8, 1/4,
-1/16), fixed halo, fused depth k (default: the plan's -- 32 in FMA mode, the
-composed-stencil kernel; ``--sweep-k`` also times k in {1,2,4,8,16,32}).
-One bench "step" = one full sweep (T=1000 time steps over the whole grid).
-At N>1 GPUs the same workload is weak-scaled: each rank owns a 2^26-point
-slab of a 2^26*N-point line, with an r*k-deep ghost exchange every launch.
-``--workload c1|c3a|c3b|c4|c5|c5f32`` runs the other BASELINE configs the same
-way (2D row slabs, 3D z-slabs of the single-GPU size per rank).
+Workload (default): BASELINE configs[4] = C5, the 3D 27-point box stencil in
+fp64 with seeded random weights, 768x768x(768*g) interior (+1 halo), T=100,
+fused depth k=2 -- the configuration the north_star's 3D targets (>= 70% of
+the fusion-depth roofline, >= 85% weak-scaling efficiency at 8 GPUs) name.
+One bench "step" = one full sweep (T time steps over the whole grid).  At
+N>1 GPUs every rank owns a 768^3 z-slab of the 768^2 x 768N grid ("weak"),
+with an r*k-deep ghost exchange (NCCL send/recv) every k steps, overlapped
+with the slab interior.  ``--scaling strong`` splits the single-GPU grid
+instead (BASELINE's C3: 16384/g rows, C4: 512/g planes).
+``--workload c1|c2|c3a|c3b|c4|c5|c5f32`` runs any BASELINE config the same way.
 
 Prints ONE JSON line (rank 0).  ``value`` = whole-job GStencil/s with the
 grid resident in HBM (CUDA events on the launching stream, max over ranks);
 ``e2e`` = the same metric through the C-ABI call with host buffers (pinned
 H2D of the input grid + sweep + D2H of the output grid, every step); at N=1
-the headline is independent grids pipelined over two plans/streams (grid
-i+1's H2D and grid i-1's D2H overlap grid i's sweep; a ring of 3 plans),
-``serial_value`` the
-three phases back to back.
+the headline is independent grids pipelined over a ring of plans/streams
+(grid i+1's H2D and grid i-1's D2H overlap grid i's sweep), ``serial_value``
+the three phases back to back.  ``roofline`` times every main launch of the
+timed region with its own CUDA events (``avg_launch_ms`` = the dominant
+kernel's mean duration) and reports BASELINE's F-based fraction and the
+executed-work fraction side by side.  ``--verify`` checks the final grid of
+the timed run against the C oracle (test infrastructure, outside the timed
+region).
 
 ``--impl reference`` times the reference's algorithm on the host CPU: the
 oracle port (oracle/oracle.c, a bit-exact C+OpenMP restatement of
@@ -43,7 +48,8 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 # BASELINE.json configs; at N > 1 every workload is weak-scaled along its
-# slowest axis (each rank owns a slab of the single-GPU size).
+# slowest axis (each rank owns a slab of the single-GPU size) unless
+# --scaling strong (the single-GPU grid split over the ranks).
 WORKLOADS = {
     "c1": dict(spec="c1", dims=(1 << 20,), T=64, name="1D3P fp64 N=2^20 T=64"),
     "c2": dict(spec="c2", dims=(1 << 26,), T=1000, name="1D5P fp64 N=2^26 T=1000"),
@@ -62,7 +68,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="c2", choices=list(WORKLOADS))
+    ap.add_argument("--workload", default="c5", choices=list(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = a single-GPU-size slab per rank; strong = the single-GPU grid split")
+    ap.add_argument("--verify", action="store_true", help="check the final grid against the C oracle")
     ap.add_argument("--k", type=int, default=0, help="fusion depth (0: the plan default -- 32 for C2 in FMA "
                                                  "mode, 4 for 2D, 2 for 3D)")
     ap.add_argument("--arith", default="fma", choices=["fma", "exact"])
@@ -276,11 +285,30 @@ def kernel_label(spec, wl, k, arith):
     return f"fused3d_kernel (K={k})"
 
 
+def executed_ops(spec, wl, k, arith, kernel_name):
+    """FP-pipe instructions per point update the main kernel's algorithm
+    issues (FMA and MUL/ADD each one op; overlapped-tile recompute excluded),
+    and a description -- the denominator of the executed-work roofline."""
+    W = len(spec.weights)
+    if arith == "exact":
+        return 2 * W - 1, "EXACT: one rounded multiply + one rounded add per term"
+    if kernel_name.startswith("compose1d"):
+        return (2 * spec.r * k + 1) / k, f"K-fold composed ({2 * spec.r * k + 1}-tap) stencil per {k} steps"
+    if kernel_name.startswith("sep_vpass"):
+        return 2 * (2 * k + 1) / k, "two composed 1D passes of 2K+1 taps per K steps"
+    if kernel_name.startswith("compose3d"):
+        return 12.5, "25-point two-step composition per 2 steps"
+    if len(wl["dims"]) == 2 and wl["spec"] == "c3a":
+        return 6, "separable push: 3 horizontal + 3 vertical FMAs per level"
+    return W, f"{W} FMA per update (one MUL + {W - 1} FMA)"
+
+
 def run_gpu_arm(args):
     import torch
     rank, world, local = dist_env()
     dist = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")           # lets the driver count communicator ranks
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")
@@ -296,7 +324,7 @@ def run_gpu_arm(args):
     dtype = wl.get("dtype", "f64")
     torch_dtype = torch.float64 if dtype == "f64" else torch.float32
     es = 8 if dtype == "f64" else 4
-    n = int(np.prod(dims))                                      # points per GPU
+    strong = args.scaling == "strong" and world > 1
     # a dedicated stream: torch's default (legacy) stream has handle 0, which
     # sb_set_stream treats as "use the plan's own stream"
     stream = torch.cuda.Stream()
@@ -306,21 +334,33 @@ def run_gpu_arm(args):
     if world > 1:
         from paper_2103_08825_b200.slab import SlabSweep
         k = k or wl.get("slab_k") or (32 if args.arith == "fma" else 16)
-        gdims = (dims[0] * world,) + dims[1:]                   # weak scaling along the slowest axis
+        gdims = dims if strong else (dims[0] * world,) + dims[1:]
         runner = SlabSweep(spec, gdims, rank=rank, world=world, k=k, arith=args.arith, dtype=dtype,
                            device=device, stream_ptr=stream.cuda_stream)
         plan = runner.plan
-        run_once = lambda: runner.run(T)                      # noqa: E731
+        n_total = int(np.prod(gdims))
     else:
         plan = Plan(spec, dims, k=k, arith=args.arith, dtype=dtype, device=device)
         k = plan.k
         plan.set_stream(stream.cuda_stream)
-        run_once = lambda: plan.launch(T)                     # noqa: E731
+        n_total = int(np.prod(dims))
+    n_local = int(np.prod(plan.dims))
     host_in = torch.empty(plan.shape, dtype=torch_dtype, pin_memory=True)
     host_in.numpy()[...] = rng.random(plan.shape)
     host_out = torch.empty_like(host_in, pin_memory=True)
     upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
     download = lambda: plan.download(host_out.numpy())       # noqa: E731
+
+    # one sweep = T steps; at N=1 every launch of the sweep is bracketed by
+    # CUDA events on the plan stream (per-launch durations of the timed region)
+    n_full, tail = divmod(T, k)
+    chunks = [k] * n_full + ([tail] if tail else [])
+
+    def sweep_events(evs):
+        for j, kk in enumerate(chunks):
+            evs[j].record(stream)
+            plan.launch(kk)
+        evs[len(chunks)].record(stream)
 
     def barrier():
         if dist is not None:
@@ -330,58 +370,77 @@ def run_gpu_arm(args):
     clocks = ClockSampler(device).start()
     upload()
     for _ in range(args.warmup):
-        run_once()
+        if world > 1:
+            runner.run(T)
+        else:
+            plan.launch(T)
     barrier()
 
+    launch_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(chunks) + 1)]
+                  for _ in range(args.steps)] if world == 1 else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     kernels_before = plan.kernel_count()
     barrier()
     clocks.mark_start()
     ev0.record(stream)
-    for _ in range(args.steps):
-        run_once()
+    for i in range(args.steps):
+        if world > 1:
+            runner.run(T)
+        else:
+            sweep_events(launch_evs[i])
     ev1.record(stream)
     barrier()
     clocks.mark_end()
     clocks.stop()
     ms = ev0.elapsed_time(ev1)
     kernels = plan.kernel_count() - kernels_before            # this rank's launches, timed region
-    launches_per_step = (T + k - 1) // k                        # main-kernel launches per sweep
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
-    value = n * world * T / (ms_per_step * 1e-3) / 1e9
+    value = n_total * T / (ms_per_step * 1e-3) / 1e9
 
-    # Dominant kernel: one main kernel per launch of k steps, average launch
-    # duration over the timed region (edge work overlaps it on a side stream).
-    launch_ms = ms_per_step / launches_per_step
+    # Dominant kernel: the main launch of k fused steps.  N=1: mean of the
+    # event-timed full-depth launches of the timed region; N>1: the step time
+    # spread over the launches (edge/interior/exchange overlap inside).
+    if world == 1:
+        full = [launch_evs[i][j].elapsed_time(launch_evs[i][j + 1])
+                for i in range(args.steps) for j in range(n_full)]
+        launch_ms = statistics.mean(full)
+        launch_src = (f"CUDA events around each of the {len(full)} full-depth (k={k}) launches of the timed "
+                      f"region, on the plan stream")
+        share = launch_ms * n_full / ms_per_step
+    else:
+        launch_ms = ms_per_step / len(chunks)
+        launch_src = "step time / launches per sweep (slab mode: edge + interior + exchange per launch)"
+        share = None
     peaks = measured_peaks()
     fp_key = "fp64" if dtype == "f64" else "fp32"
     fp_peak = peaks[f"{fp_key}_tflops"]
     per_gpu = value / world
-    flops_per_update = 2 * len(spec.weights) - 1            # BASELINE's F = 2|W| - 1
+    F = 2 * len(spec.weights) - 1                             # BASELINE's F = 2|W| - 1
     alg_bytes_per_point = 2 * es                              # read + write once per fused launch
-    fp_bound = fp_peak * 1e12 / flops_per_update / 1e9
+    fp_bound = fp_peak * 1e12 / F / 1e9
     hbm_bound = peaks["hbm_gbs"] * 1e9 * k / alg_bytes_per_point / 1e9
     binding = "hbm" if hbm_bound < fp_bound else fp_key
-    composed1d = len(dims) == 1 and args.arith == "fma" and k >= 16    # compose1d_kernel (launch1d.cu)
     kernel_name = kernel_label(spec, wl, k, args.arith)
-    # algorithmic work per launch of k steps: 2s B per point (read + write once),
-    # F flops per point update
-    alg_bytes = alg_bytes_per_point * n
-    alg_flops = flops_per_update * n * k
+    # algorithmic work per launch of k steps: 2s B per point
+    # (read + write once), F flops per point update
+    alg_bytes = alg_bytes_per_point * n_local
+    alg_flops = F * n_local * k
     achieved_gbs = alg_bytes / (launch_ms * 1e-3) / 1e9
-    achieved_tflops = per_gpu * 1e9 * flops_per_update / 1e12   # = alg_flops / launch time
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "r01_bench_kernel_traffic.json")
+    achieved_tflops = alg_flops / (launch_ms * 1e-3) / 1e12
+    traffic, traffic_src = None, None
+    tpath = os.path.join(REPO, "profiles", "kernel_traffic.json")
     if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             tj = json.load(fh)
-        if composed1d and kernel_name in tj["kernel"] and args.workload == "c2":   # same kernel and grid
-            traffic = tj["traffic_bytes"]
+        ent = tj.get(f"{args.workload}:{args.arith}:k{k}")
+        if ent and ent.get("dims") == list(dims):
+            traffic = ent["traffic_bytes"]
+            traffic_src = ent["source"]
     hbm_view = {"achieved": achieved_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved_gbs / peaks["hbm_gbs"], "alg_bytes_per_launch": alg_bytes,
                 "peak_source": peaks["source"]["hbm"]}
@@ -389,12 +448,21 @@ def run_gpu_arm(args):
                "frac": achieved_tflops / fp_peak, "alg_flops_per_launch": alg_flops,
                "peak_source": peaks["source"][fp_key]}
     main = hbm_view if binding == "hbm" else fp_view
+    ops, ops_desc = executed_ops(spec, wl, k, args.arith, kernel_name)
+    exec_fp_bound = fp_peak * 1e12 / 2 / ops / 1e9           # pipe ops/s (an FMA = 2 flops of the peak)
+    exec_bound = min(hbm_bound, exec_fp_bound)
+    kern_rate = n_local * k / (launch_ms * 1e-3) / 1e9       # dominant kernel alone, GStencil/s
     roofline = {
         "bound": binding, "achieved": main["achieved"], "peak": main["peak"], "unit": main["unit"],
-        "frac": main["frac"], "traffic": traffic,
-        "traffic_source": "profiles/r01_bench_kernel_traffic.json (ncu --set full, one launch: "
-                          "dram__bytes_read.sum + dram__bytes_write.sum; C2 only, else null)",
-        "kernel": kernel_name, "avg_launch_ms": launch_ms,
+        "frac": main["frac"], "traffic": traffic, "traffic_source": traffic_src,
+        "kernel": kernel_name, "avg_launch_ms": launch_ms, "avg_launch_source": launch_src,
+        "kernel_share_of_step": share,
+        "executed_frac": kern_rate / exec_bound,
+        "executed": {"fp_ops_per_update": ops, "what": ops_desc,
+                     "roofline_gstencil": exec_bound, "kernel_gstencil": kern_rate,
+                     "fp_pipe_frac": kern_rate * 1e9 * ops * 2 / (fp_peak * 1e12),
+                     "note": "executed_frac = the dominant kernel's rate / min(HBM bound, FP peak over the "
+                             "FP-pipe ops its algorithm issues); 'frac' uses BASELINE's F = 2|W|-1 flops"},
         "note": f"bound = the lower of the HBM roofline ({alg_bytes_per_point} B/point/launch) and the "
                 f"{fp_key.upper()} roofline (F flops/update); '{fp_key}' is the CUDA-core {fp_key.upper()} "
                 "pipe (a stencil is not a tensor-core contraction)",
@@ -404,33 +472,10 @@ def run_gpu_arm(args):
         "k": k, "hbm_bound_gstencil": hbm_bound, f"{fp_key}_bound_gstencil": fp_bound,
         "binding": binding, "achieved_gstencil_per_gpu": per_gpu,
         "frac": per_gpu / min(hbm_bound, fp_bound),
-        "note": "frac uses BASELINE's algorithmic F = 2|W|-1 flops per update",
+        "executed_frac": per_gpu / exec_bound,
+        "note": "frac uses BASELINE's algorithmic F = 2|W|-1 flops per update; executed_frac the "
+                "FP-pipe ops the kernel's algorithm issues (roofline.executed)",
     }
-    if composed1d:
-        # composed-stencil path: (2RK+1) FMAs per point per launch of k steps
-        fma_per_update = (2 * spec.r * k + 1) / k
-        fma_rate = per_gpu * 1e9 * fma_per_update
-        stencil_roofline["executed"] = {
-            "kernel": "compose1d_kernel (K-fold composed (2RK+1)-tap stencil)",
-            "fma_per_update": fma_per_update,
-            "fp64_fma_rate_tflops": 2 * fma_rate / 1e12,
-            "fp64_pipe_frac": 2 * fma_rate / (peaks["fp64_tflops"] * 1e12),
-        }
-    elif kernel_name.startswith("sep_vpass"):
-        fma_per_update = 2 * (2 * k + 1) / k                  # two composed 1D passes
-        fma_rate = per_gpu * 1e9 * fma_per_update
-        stencil_roofline["executed"] = {
-            "kernel": kernel_name, "fma_per_update": fma_per_update,
-            "fp64_fma_rate_tflops": 2 * fma_rate / 1e12,
-            "fp64_pipe_frac": 2 * fma_rate / (peaks["fp64_tflops"] * 1e12),
-        }
-    elif kernel_name.startswith("compose3d"):
-        fma_rate = per_gpu * 1e9 * 12.5                       # 25 FMAs per point per two steps
-        stencil_roofline["executed"] = {
-            "kernel": kernel_name, "fma_per_update": 12.5,
-            "fp64_fma_rate_tflops": 2 * fma_rate / 1e12,
-            "fp64_pipe_frac": 2 * fma_rate / (peaks["fp64_tflops"] * 1e12),
-        }
 
     # End to end through the C-ABI with host buffers: every step uploads its
     # input grid from pinned host memory (H2D), sweeps T steps and downloads
@@ -439,6 +484,7 @@ def run_gpu_arm(args):
     # their own streams (sb_upload_async / sb_launch / sb_download_async), so
     # grid i+1's H2D and grid i-1's D2H run on the copy engines during grid i's sweep.
     e2e = None
+    run_once = (lambda: runner.run(T)) if world > 1 else (lambda: plan.launch(T))   # noqa: E731
     if not args.no_e2e:
         barrier()
         t0 = time.perf_counter()
@@ -452,7 +498,7 @@ def run_gpu_arm(args):
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-        serial = n * world * T * args.steps / dt / 1e9
+        serial = n_total * T * args.steps / dt / 1e9
         e2e = {"value": serial, "unit": "GStencil/s",
                "h2d_bytes_per_step": int(host_in.numel() * es * world),
                "d2h_bytes_per_step": int(host_out.numel() * es * world),
@@ -487,11 +533,33 @@ def run_gpu_arm(args):
             same = all(np.array_equal(o.numpy(), want) for o in outs)
             for p in plans[1:]:
                 p.close()
-            e2e.update({"value": n * T * args.steps / dt / 1e9, "mode": "pipelined",
+            e2e.update({"value": n_total * T * args.steps / dt / 1e9, "mode": "pipelined",
                         "serial_value": serial, "result_matches_serial": bool(same),
                         "timer": f"host wall clock from the first enqueue to every plan's sync; "
                                  f"{args.steps} independent grids over a ring of {NP} plans/streams "
                                  f"(includes the unoverlapped first H2D and last D2H)"})
+
+    verify = None
+    if args.verify and world == 1:
+        # the bench path's output for one sweep of host_in vs the C oracle (test
+        # infrastructure; outside every timed region)
+        from oracle import c_oracle
+        from paper_2103_08825_b200.core import canonical
+        offs, ws = canonical(spec)
+        upload()
+        plan.launch(T)
+        download()
+        torch.cuda.synchronize()
+        o_in = host_in.numpy().astype(np.float64)
+        o_ws = [float(np.float32(w)) for w in ws] if dtype == "f32" else ws
+        t0 = time.perf_counter()
+        want = c_oracle.sweep(o_in, spec.r, offs, o_ws, T, inplace=True)
+        g = host_out.numpy().astype(np.float64)
+        err = float(np.max(np.abs(g - want) / np.maximum(np.abs(want), np.finfo(np.float64).tiny)))
+        tol = 1e-5 if dtype == "f32" else (0.0 if args.arith == "exact" else 1e-12)
+        verify = {"max_rel_err": err, "tol": tol, "ok": bool(err <= tol), "T": T,
+                  "oracle": f"oracle/oracle.c on {c_oracle.max_threads()} threads, "
+                            f"{time.perf_counter() - t0:.1f} s"}
 
     sweep = None
     if args.sweep_k and world == 1:
@@ -502,7 +570,7 @@ def run_gpu_arm(args):
                 p.upload(host_in.numpy())
                 p.run(T // 4)
                 tim = p.run(T)
-                g = n * T / (tim.device_ms * 1e-3) / 1e9
+                g = n_local * T / (tim.device_ms * 1e-3) / 1e9
                 hb = peaks["hbm_gbs"] * kk / alg_bytes_per_point
                 sweep[str(kk)] = {"gstencil": g, "ms": tim.device_ms, "launches": tim.launches,
                                   "kernel": tim.kernel_name, "roofline_gstencil": min(hb, fp_bound),
@@ -518,22 +586,27 @@ def run_gpu_arm(args):
                                   + (", fp64 (the reference is fp64-only)" if dtype == "f32" else "")}
         if len(dims) == 1:
             try:
-                cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n)
+                cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n_local)
             except MemoryError:
                 pass
 
     if rank == 0:
-        grid_bytes = int(np.prod([d + 2 * spec.r for d in dims])) * es
+        grid_bytes = int(np.prod([d + 2 * spec.r for d in plan.dims])) * es
+        if world > 1:
+            scale = (f", strong-scaled over {world} GPUs (1/{world} slab per GPU)" if strong
+                     else f", weak-scaled x{world} (a single-GPU-size slab per GPU)")
+        else:
+            scale = ""
         line = {
             "metric": "GStencil/s", "value": value, "unit": "GStencil/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
-            "config": {"workload": wl["name"] + (f", weak-scaled x{world} (slab per GPU)" if world > 1 else ""),
-                       "k": k, "arith": args.arith, "grid_bytes": grid_bytes,
+            "config": {"workload": wl["name"] + scale, "dims_per_gpu": list(plan.dims),
+                       "k": k, "arith": args.arith, "grid_bytes_per_gpu": grid_bytes,
                        "l2": (f"inputs larger than L2 ({grid_bytes / 1e6:.0f} MB grid vs 126 MB L2)"
                               if grid_bytes > (126 << 20) else "grid fits in L2"),
-                       "parallelism": f"slab{world}" if world > 1 else "single"},
+                       "parallelism": (f"slab{world}" if world > 1 else "single")},
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels * world,
@@ -542,6 +615,8 @@ def run_gpu_arm(args):
                                  "boundary kernel / the 3D shell kernel on a side stream",
             "clocks": clocks.summary(),
         }
+        if verify is not None:
+            line["verify"] = verify
         if sweep is not None:
             line["k_sweep"] = sweep
         print(json.dumps(line), flush=True)

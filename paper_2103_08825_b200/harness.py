@@ -138,7 +138,7 @@ def seed_grid(cfg: BenchConfig, spec: StencilSpec):
     return grid
 
 
-def _execute(cfg: BenchConfig, spec: StencilSpec, counters: Counters):
+def _execute(cfg: BenchConfig, spec: StencilSpec, counters: Counters, arith: str = "exact"):
     from . import transpose as tr
     layout = B200_METHODS[cfg.method]
     grid = seed_grid(cfg, spec)
@@ -148,7 +148,7 @@ def _execute(cfg: BenchConfig, spec: StencilSpec, counters: Counters):
         t0 = time.perf_counter()
         (tr.to_block_transpose if layout is Layout.BLOCK_TRANSPOSE else tr.to_dlt)(grid, cfg.vl)
         layout_s += time.perf_counter() - t0
-    b200_sweep(grid, spec, cfg.jam_k, cfg.steps, counters, arith="exact")
+    b200_sweep(grid, spec, cfg.jam_k, cfg.steps, counters, arith=arith)
     if layout is not Layout.NATURAL:
         t0 = time.perf_counter()
         (tr.from_block_transpose if layout is Layout.BLOCK_TRANSPOSE else tr.from_dlt)(grid)
@@ -161,19 +161,20 @@ def max_rel_error(got: np.ndarray, want: np.ndarray) -> float:
     return float(np.max(np.abs(got - want) / denom))
 
 
-def run_benchmark(cfg: BenchConfig, oracle=None) -> BenchResult:
+def run_benchmark(cfg: BenchConfig, oracle=None, arith: str = "exact") -> BenchResult:
     """One configuration: timing, counters, and with ``cfg.verify`` the max
     relative error against ``oracle(cfg, spec) -> natural interior`` (the
-    caller's reference, e.g. ``stencilbench.harness.run_oracle``)."""
+    caller's reference, e.g. ``stencilbench.harness.run_oracle``).
+    ``arith`` 'exact' (default, bit-identical) or 'fma'."""
     validate_config(cfg)
     spec = cfg.spec()
     if cfg.verify and oracle is None:
         raise UsageError("--verify needs the reference oracle (run_benchmark(cfg, oracle=...))")
     warm = BenchConfig(cfg.stencil, (1,) * (spec.d - 1) + (max(16, 8 * spec.r),), 1, cfg.method,
                        vl=cfg.vl, jam_k=1, seed=cfg.seed, weights=cfg.weights)
-    _execute(warm, spec, Counters())                      # harness.py:165-172
+    _execute(warm, spec, Counters(), arith)               # harness.py:165-172
     counters = Counters()
-    result, total_s, layout_s = _execute(cfg, spec, counters)
+    result, total_s, layout_s = _execute(cfg, spec, counters, arith)
     gflops = counters.point_updates * flops_per_point(spec) / max(total_s, 1e-12) / 1e9
     err = max_rel_error(result, oracle(cfg, spec)) if cfg.verify else None
     return BenchResult(cfg, total_s, layout_s, gflops, counters, err)
