@@ -35,6 +35,10 @@ def up_to_date() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    global LIB_DIR, LIB
+    if os.environ.get("SB200_BUILD_DIR"):   # development: variant library elsewhere (load with SB200_LIB)
+        LIB_DIR = os.environ["SB200_BUILD_DIR"]
+        LIB = os.path.join(LIB_DIR, "libsb200.so")
     if not force and up_to_date():
         return LIB
     os.makedirs(LIB_DIR, exist_ok=True)
@@ -44,6 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not os.path.exists(nvcc):
         nvcc = "nvcc"
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+    extra = os.environ.get("SB200_NVCC_EXTRA", "").split()   # development: variant builds (with SB200_BUILD_DIR)
+    flags += extra
     procs, objs = [], []
     for src in SOURCES:
         obj = os.path.join(obj_dir, src.replace(".cu", ".o"))

@@ -6,6 +6,7 @@
 #include "plan.hpp"
 #include "fused3d.cuh"
 #include "compose3d.cuh"
+#include "box3d.cuh"
 
 namespace sbh {
 namespace {
@@ -18,7 +19,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 // One TMA descriptor per device buffer: a 3D view (cols, rows, planes) of
 // the whole allocation; boxes of F3_PW x (region height + 2) x 1, OOB elements zero-filled.
-int make_tensor_maps_impl(sb_plan* P, int geo, int box_h) {
+int make_tensor_maps_impl(sb_plan* P, int geo, int box_h, int box_w = sb::F3_PW) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     SB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
@@ -28,13 +29,21 @@ int make_tensor_maps_impl(sb_plan* P, int geo, int box_h) {
     const int64_t planes = P->hlo + P->dims[0] + P->hhi;
     cuuint64_t dims[3] = {(cuuint64_t)P->px, (cuuint64_t)rows, (cuuint64_t)planes};
     cuuint64_t strides[2] = {(cuuint64_t)(P->px * P->es), (cuuint64_t)(rows * P->px * P->es)};
-    cuuint32_t box[3] = {(cuuint32_t)sb::F3_PW, (cuuint32_t)box_h, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     const CUtensorMapDataType dt = P->dtype == SB_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    // box3d (geometries 4-6) reads 68-wide boxes that start 16 B before a 128 B line:
+    // 64 B promotion fetched 10% fewer DRAM bytes than 128 B (4.89 vs 5.44 GB per C5
+    // launch) and ran 1% faster; the other 3D kernels keep 128 B
+    static const int promo_env = (int)env_double("SB200_TMA_L2PROMO", -1);
+    const int promo = promo_env >= 0 ? promo_env : (geo >= 4 ? 64 : 128);
+    const CUtensorMapL2promotion pr = promo == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
     for (int b = 0; b < 2; b++) {
         CUresult r = encode(&P->tmap[geo][b], dt, 3, P->buf[b], dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                            CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SB_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     }
     P->tmap_ok[geo] = true;
@@ -282,10 +291,102 @@ int launch_compose3d_t(sb_plan* P, int src_idx) {
     return launch_compose3d<T, 4, 4>(P, src_idx);
 }
 
+// ---- 27-point box, k = 2: output tiles of exactly 64 x TY, ring-only
+// level-1 recompute (box3d.cuh)
+
+template <typename T, bool FMA, int NW, int MINB, bool U3 = false, bool SKEW = false>
+int launch_box3d(sb_plan* P, int src_idx) {
+    using G = sb::B3Geo<T, NW>;
+    constexpr int GEO = NW == 4 ? 4 : (NW == 8 ? 5 : 6);   // tensor-map slot of this box geometry
+    if (!P->tmap_ok[GEO]) {
+        const int rc = make_tensor_maps_impl(P, GEO, G::PH, G::PW);
+        if (rc != SB_OK) return rc;
+    }
+    auto kern = sb::box3d_kernel<T, FMA, NW, MINB, U3, SKEW>;
+    SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
+    int occ = 0;
+    SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::THREADS, G::SMEM));
+    occ = std::max(occ, 1);
+    sb::Box3DParams<T> prm;
+    prm.src = reinterpret_cast<const T*>(P->buf[src_idx]);
+    prm.dst = reinterpret_cast<T*>(P->buf[src_idx ^ 1]);
+    prm.origin = P->g.origin;
+    prm.sz = P->g.sz;
+    prm.sy = P->g.sy;
+    prm.nz = (int)P->dims[0];
+    prm.ny = (int)P->dims[1];
+    prm.nx = (int)P->dims[2];
+    prm.ax = (int)(P->g.origin % P->g.sy);
+    prm.ry = P->r;
+    prm.hz = (int)P->hlo;
+    prm.hz_hi = (int)P->hhi;
+    prm.phys_lo = P->phys_lo;
+    prm.phys_hi = P->phys_hi;
+    prm.tiles_x = (int)((P->dims[2] + 63) / 64);
+    prm.tiles_y = (int)((P->dims[1] + G::TY - 1) / G::TY);
+    const int ctas_max = P->num_sms * occ;
+    const int tiles = prm.tiles_x * prm.tiles_y;
+    const double per = env_double("SB200_B3_ITEMS_PER_CTA", 8.0);
+    const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
+    const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
+    prm.lz = (int)((nzr + nseg - 1) / nseg);
+    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
+    prm.z0 = (int)z_lo;
+    prm.z1 = (int)(z_lo + nzr);
+    prm.items = tiles * prm.nseg;
+    prm.total_ctas = std::min(ctas_max, prm.items);
+    prm.counter = P->d_counter;
+    static const int split = (int)env_double("SB200_B3_SPLIT", 0);
+    prm.split = prm.tiles_x >= 2 ? split : 0;
+    prm.num_sms = P->num_sms;
+    prm.q_items[0] = (prm.tiles_x / 2) * prm.tiles_y * prm.nseg;
+    prm.q_items[1] = (prm.tiles_x - prm.tiles_x / 2) * prm.tiles_y * prm.nseg;
+    for (int i = 0; i < 27; i++) prm.w[i] = T(0);
+    for (int i = 0; i < P->nw; i++) {
+        const int* o = &P->offsets[3 * i];
+        prm.w[(o[0] + 1) * 9 + (o[1] + 1) * 3 + (o[2] + 1)] = (T)P->weights[i];
+    }
+    for (int i = 0; i < 27; i++) {   // fp32 packed push: (w, w)
+        const float f = (float)prm.w[i];
+        unsigned int u;
+        memcpy(&u, &f, 4);
+        prm.wpp[i] = ((unsigned long long)u << 32) | u;
+    }
+    P->last_kernel = "box3d_kernel";
+    kern<<<(unsigned)prm.total_ctas, G::THREADS, G::SMEM, P->stream>>>(P->tmap[GEO][src_idx], prm);
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+template <typename T, bool FMA>
+int launch_box3d_t(sb_plan* P, int src_idx) {
+    static const int nw = (int)env_double("SB200_B3_NW", 4);
+    static const int minb = (int)env_double("SB200_B3_MINB", 0);
+    static const int u3 = (int)env_double("SB200_B3_U3", 0);
+    if constexpr (sizeof(T) == 4 && FMA) {
+        if (u3 && nw == 4) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
+    }
+    static const int skew = (int)env_double("SB200_B3_SKEW", 0);
+    if (skew && nw == 4) return launch_box3d<T, FMA, 4, 4, false, true>(P, src_idx);
+    if (skew && nw == 8) return launch_box3d<T, FMA, 8, 2, false, true>(P, src_idx);
+    if (nw == 3) return launch_box3d<T, FMA, 3, 5>(P, src_idx);
+    if (nw == 4 && minb == 3) return launch_box3d<T, FMA, 4, 3>(P, src_idx);
+    if (nw == 4) return launch_box3d<T, FMA, 4, 4>(P, src_idx);
+    return launch_box3d<T, FMA, 8, 2>(P, src_idx);
+}
+
+bool box3d_ok(const sb_plan* P, int k) {
+    static const int enabled = (int)env_double("SB200_B3", 1);
+    return enabled && k == 2 && P->shape == SB_BOX && P->nw == 27;
+}
+
 template <typename T, bool BOX, bool FMA>
 int launch_fused3d_b(sb_plan* P, int src_idx, int k) {
     if constexpr (!BOX && FMA) {
         if (compose3d_ok(P, k)) return launch_compose3d_t<T>(P, src_idx);
+    }
+    if constexpr (BOX) {
+        if (box3d_ok(P, k)) return launch_box3d_t<T, FMA>(P, src_idx);
     }
     switch (k) {
         case 1: return launch_fused3d_k<T, BOX, 1, FMA>(P, src_idx);

@@ -87,8 +87,8 @@ struct sb_plan {
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<sbh::Sched1D> sched1d;
     std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
-    CUtensorMap tmap[4][2];                // TMA descriptors [geometry][buffer] (3D; 2, 3: composed)
-    bool tmap_ok[4] = {false, false, false, false};
+    CUtensorMap tmap[8][2];                // TMA descriptors [geometry][buffer] (3D; 2, 3: composed; 4-6: box3d)
+    bool tmap_ok[8] = {false, false, false, false, false, false, false, false};
     void* tmp = nullptr;                   // scratch grid of the separable composed 2D path
     void* stage = nullptr;                 // reference-storage staging rows (sb_upload_storage)
     size_t stage_bytes = 0;
