@@ -197,6 +197,31 @@ int sb_download_storage(sb_plan *plan, void *host, size_t bytes, const sb_storag
 int sb_layout_convert(void *dst, const void *src, int64_t rows, const sb_storage *st, int32_t to_layout,
                       int32_t dtype, void *stream);
 
+/* ---- single-process multi-GPU sweep (grid in, grid out over `ngpu` devices)
+ *
+ * The interior is split along the slowest axis into `ngpu` balanced slabs,
+ * one slab plan per device (`devices[i]`, NULL = 0 .. ngpu-1; a device may
+ * repeat, e.g. to emulate the decomposition on one GPU).  Every slab carries
+ * G = r*k ghost planes per side facing another slab; between launches of k
+ * fused steps the new edge planes are peer-copied (NVLink, copy streams)
+ * into the neighbours' ghost planes, overlapped with the slab interiors
+ * (2D/3D).  Results are bit-identical to one device.  Host boxes are the
+ * GLOBAL compact halo-inclusive box.  Replaces, for a multi-GPU node, the
+ * whole-grid sweep of sb_plan_create/sb_upload/sb_run/sb_download.  */
+typedef struct sb_multi sb_multi;
+int sb_multi_create(sb_multi **multi, const sb_problem *problem, int32_t ngpu, const int32_t *devices);
+void sb_multi_destroy(sb_multi *multi);
+int sb_multi_upload(sb_multi *multi, const void *host, size_t bytes);
+int sb_multi_download(sb_multi *multi, void *host, size_t bytes);
+/* Advance `steps` steps (synchronous); timing->device_ms = max over devices. */
+int sb_multi_run(sb_multi *multi, int64_t steps, sb_timing *timing);
+int sb_multi_info(const sb_multi *multi, int32_t *ngpu, int32_t *k);
+/* Slab i: global interior planes [start, end) on `device`. */
+int sb_multi_slab(const sb_multi *multi, int32_t i, int64_t *start, int64_t *end, int32_t *device);
+
+/* Fused depth a plan for `problem` would use (host only, no device needed). */
+int sb_problem_k(const sb_problem *problem, int32_t *k);
+
 /* Fused depth the plan will use per launch. */
 int sb_plan_k(const sb_plan *plan, int32_t *k);
 

@@ -24,7 +24,9 @@ EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_download", "sb_run", "sb_launch", "sb_set_stream", "sb_device_view",
            "sb_plan_k", "sb_kernel_count", "sb_last_error", "sb_abi_version", "sb_device_count",
            "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
-           "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range")
+           "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
+           "sb_multi_create", "sb_multi_destroy", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
+           "sb_multi_info", "sb_multi_slab", "sb_problem_k")
 
 
 class SbProblem(ctypes.Structure):
@@ -90,6 +92,17 @@ def load():
     lib.sb_download_storage.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, SP]
     lib.sb_layout_convert.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, SP, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.c_void_p]
+    lib.sb_multi_create.argtypes = [ctypes.POINTER(P), ctypes.POINTER(SbProblem), ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_int32)]
+    lib.sb_multi_destroy.argtypes = [P]
+    lib.sb_multi_destroy.restype = None
+    lib.sb_multi_upload.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
+    lib.sb_multi_download.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
+    lib.sb_multi_run.argtypes = [P, ctypes.c_int64, ctypes.POINTER(SbTiming)]
+    lib.sb_multi_info.argtypes = [P, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
+    lib.sb_multi_slab.argtypes = [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.POINTER(ctypes.c_int32)]
+    lib.sb_problem_k.argtypes = [ctypes.POINTER(SbProblem), ctypes.POINTER(ctypes.c_int32)]
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_last_error.argtypes = []
     lib.sb_abi_version.restype = ctypes.c_int
@@ -97,7 +110,9 @@ def load():
     for name in ("sb_plan_create", "sb_host_elems", "sb_upload", "sb_download", "sb_run",
                  "sb_launch", "sb_set_stream", "sb_device_view", "sb_plan_k", "sb_kernel_count",
                  "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
-                 "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range"):
+                 "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
+                 "sb_multi_create", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
+                 "sb_multi_info", "sb_multi_slab", "sb_problem_k"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

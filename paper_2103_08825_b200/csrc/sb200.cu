@@ -404,13 +404,9 @@ void sb_plan_destroy(sb_plan* P) {
     delete P;
 }
 
-int sb_plan_create(sb_plan** out, const sb_problem* prob) {
-    if (!out) return fail(SB_ERR_ARG, "plan output pointer is NULL");
-    *out = nullptr;
-    int rc = validate_problem(prob);
-    if (rc != SB_OK) return rc;
-    sb_plan* P = new (std::nothrow) sb_plan();
-    if (!P) return fail(SB_ERR_NOMEM, "host allocation failed");
+// Host-side fields of a plan and its kernel choice / fused depth (no device
+// resources); shared by sb_plan_create and sb_problem_k.
+static int plan_host_setup(sb_plan* P, const sb_problem* prob) {
     P->d = prob->d;
     P->r = prob->r;
     P->shape = prob->shape;
@@ -432,14 +428,12 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     // ---- kernel choice
     const int fk = fused_kind(P);
     if (prob->kernel == SB_KERNEL_FUSED && !fk) {
-        delete P;
         return fail(SB_ERR_ARG, "no fused kernel for d=%d r=%d shape=%d", prob->d, prob->r, prob->shape);
     }
     if (prob->kernel != SB_KERNEL_GENERIC && fk) {
         P->kind = fk;
         P->k = prob->k > 0 ? prob->k : default_k(fk, P);
         if (!fused_k_ok(P, fk, P->k)) {
-            delete P;
             return fail(SB_ERR_ARG, "fused depth k=%d unsupported by the %s kernel", prob->k,
                         fk == KK_FUSED3D ? "3D (1..4)" : fk == KK_FUSED2D ? "2D (1, 2, 4, 8)"
                         : "1D (1, 2, 4, 8, 16; 32, 64 in FMA mode with r*k <= 64)");
@@ -447,6 +441,32 @@ int sb_plan_create(sb_plan** out, const sb_problem* prob) {
     } else {
         P->kind = KK_GENERIC;
         P->k = 1;
+    }
+    return SB_OK;
+}
+
+int sb_problem_k(const sb_problem* prob, int32_t* k) {
+    if (!k) return fail(SB_ERR_ARG, "NULL argument");
+    int rc = validate_problem(prob);
+    if (rc != SB_OK) return rc;
+    sb_plan tmp;
+    rc = plan_host_setup(&tmp, prob);
+    if (rc != SB_OK) return rc;
+    *k = tmp.k;
+    return SB_OK;
+}
+
+int sb_plan_create(sb_plan** out, const sb_problem* prob) {
+    if (!out) return fail(SB_ERR_ARG, "plan output pointer is NULL");
+    *out = nullptr;
+    int rc = validate_problem(prob);
+    if (rc != SB_OK) return rc;
+    sb_plan* P = new (std::nothrow) sb_plan();
+    if (!P) return fail(SB_ERR_NOMEM, "host allocation failed");
+    rc = plan_host_setup(P, prob);
+    if (rc != SB_OK) {
+        delete P;
+        return rc;
     }
     if (!(P->phys_lo && P->phys_hi)) {
         // slab: a launch of depth k needs ghost depth >= r*k on slab sides

@@ -233,6 +233,112 @@ def storage_descriptor(grid) -> _abi.SbStorage:
     return st
 
 
+def _problem(spec, dims, dtype, arith, k, kernel, device, ghost=(0, 0)):
+    """(sb_problem, keep-alive arrays) for a spec over interior ``dims``."""
+    offs, ws = canonical(spec)
+    d = spec.d
+    c_offs = (ctypes.c_int32 * (len(offs) * d))(*[c for o in offs for c in o])
+    c_ws = (ctypes.c_double * len(ws))(*ws)
+    prob = _abi.SbProblem()
+    prob.d, prob.r = d, spec.r
+    prob.shape = _abi.SB_STAR if spec.shape == "star" else _abi.SB_BOX
+    prob.nw = len(ws)
+    prob.offsets = ctypes.cast(c_offs, ctypes.POINTER(ctypes.c_int32))
+    prob.weights = ctypes.cast(c_ws, ctypes.POINTER(ctypes.c_double))
+    for a in range(3):
+        prob.dims[a] = int(dims[a]) if a < d else 1
+    prob.dtype = _DTYPES[dtype][0]
+    prob.arith = _ARITH[arith]
+    prob.k = int(k)
+    prob.kernel = _KERNEL[kernel]
+    prob.device = int(device)
+    prob.ghost_lo, prob.ghost_hi = ghost
+    return prob, (c_offs, c_ws)
+
+
+class MultiPlan:
+    """One grid over several GPUs of this node (include/sb200.h sb_multi_*).
+
+    The interior is split along the slowest axis into ``ngpu`` slabs, one
+    slab plan per device of ``devices`` (default 0 .. ngpu-1; repeating a
+    device emulates the decomposition on one GPU).  Ghost planes (depth r*k)
+    are peer-copied between neighbours after every launch of k fused steps,
+    overlapped with the slab interiors; the result is bit-identical to one
+    device.  Host boxes are the GLOBAL compact halo-inclusive box.
+    """
+
+    def __init__(self, spec, dims, *, ngpu, devices=None, dtype="f64", arith="fma", k=0, kernel="auto"):
+        validate(spec)
+        if dtype not in _DTYPES or arith not in _ARITH or kernel not in _KERNEL:
+            raise ValueError("bad dtype / arith / kernel")
+        self.spec = spec
+        self.d, self.r = spec.d, spec.r
+        self.dims = tuple(int(n) for n in dims)
+        if len(self.dims) != self.d:
+            raise GridError(f"{getattr(spec, 'name', 'spec')} needs {self.d} extents, got {len(self.dims)}")
+        self.np_dtype = _DTYPES[dtype][1]
+        self.shape = host_shape(self.d, self.r, self.dims)
+        prob, self._keep = _problem(spec, self.dims, dtype, arith, k, kernel, 0)
+        devs = list(range(ngpu)) if devices is None else [int(x) for x in devices]
+        if len(devs) != ngpu:
+            raise ValueError(f"devices has {len(devs)} entries, ngpu is {ngpu}")
+        c_devs = (ctypes.c_int32 * ngpu)(*devs)
+        self._lib = _abi.load()
+        h = ctypes.c_void_p()
+        _abi.check(self._lib.sb_multi_create(ctypes.byref(h), ctypes.byref(prob), int(ngpu), c_devs))
+        self._h = h
+        g, kk = ctypes.c_int32(), ctypes.c_int32()
+        _abi.check(self._lib.sb_multi_info(self._h, ctypes.byref(g), ctypes.byref(kk)))
+        self.ngpu, self.k = int(g.value), int(kk.value)
+
+    def slabs(self):
+        """[(start, end, device)] of every slab (global interior planes)."""
+        out = []
+        for i in range(self.ngpu):
+            a, b, dv = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+            _abi.check(self._lib.sb_multi_slab(self._h, i, ctypes.byref(a), ctypes.byref(b), ctypes.byref(dv)))
+            out.append((int(a.value), int(b.value), int(dv.value)))
+        return out
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._lib.sb_multi_destroy(h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check_box(self, box):
+        if box.shape != self.shape or box.dtype != self.np_dtype or not box.flags.c_contiguous:
+            raise GridError(f"host box must be C-contiguous {np.dtype(self.np_dtype)} of shape {self.shape}")
+
+    def upload(self, box: np.ndarray) -> None:
+        self._check_box(box)
+        _abi.check(self._lib.sb_multi_upload(self._h, box.ctypes.data, box.nbytes))
+
+    def download(self, out: np.ndarray | None = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.shape, dtype=self.np_dtype)
+        self._check_box(out)
+        _abi.check(self._lib.sb_multi_download(self._h, out.ctypes.data, out.nbytes))
+        return out
+
+    def run(self, steps: int) -> Timing:
+        t = _abi.SbTiming()
+        _abi.check(self._lib.sb_multi_run(self._h, int(steps), ctypes.byref(t)))
+        return Timing(t.device_ms, t.kernel_ms, t.launches, t.point_updates, t.k_used, t.kernel_name.decode())
+
+
 _CACHE = threading.local()
 PLAN_CACHE_SIZE = 8     # plans kept per host thread (device memory stays allocated)
 
@@ -274,11 +380,13 @@ def clear_plan_cache() -> None:
 
 
 def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
-          device=0, dtype=None) -> np.ndarray:
+          device=0, dtype=None, ngpu=1, devices=None) -> np.ndarray:
     """``steps`` Jacobi steps of ``spec`` over a compact halo-inclusive ``box``.
 
     Returns a new box (halo preserved).  The grid-in/grid-out entry point of
     the drop-in (stencil shape and coefficients, input grid, timestep count).
+    ``ngpu`` > 1 splits the grid into slabs over that many devices of this
+    node (``devices``: their ordinals, default 0 .. ngpu-1) -- see MultiPlan.
     """
     validate(spec)
     box = np.asarray(box)
@@ -290,10 +398,16 @@ def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
     dims = tuple(s - 2 * spec.r for s in box.shape)
     if any(n <= 0 for n in dims):
         raise GridError(f"box shape {box.shape} too small for order {spec.r}")
+    if ngpu > 1 or devices is not None:
+        n = ngpu if devices is None else len(devices)
+        with MultiPlan(spec, dims, ngpu=n, devices=devices, dtype=dtype, arith=arith, k=k, kernel=kernel) as p:
+            p.upload(np.ascontiguousarray(box, dtype=np_dtype))
+            p.run(steps)
+            return p.download()
     with Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device) as p:
         p.upload(np.ascontiguousarray(box, dtype=np_dtype))
         p.run(steps)
         return p.download()
 
 
-__all__ = ["Plan", "Timing", "sweep", "cached_plan", "clear_plan_cache", "host_shape", "storage_descriptor", "SpecError", "GridError"]
+__all__ = ["Plan", "MultiPlan", "Timing", "sweep", "cached_plan", "clear_plan_cache", "host_shape", "storage_descriptor", "SpecError", "GridError"]

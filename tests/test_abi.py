@@ -116,3 +116,32 @@ def test_c_client_bit_identical_on_device(lib, tmp_path):
     exe = _build_c_client(tmp_path)
     r = subprocess.run([exe, "300007", "37"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and r.stdout.startswith("bit-identical"), r.stdout + r.stderr
+
+
+def _config_problem(key, dims, arith, k=0):
+    from paper_2103_08825_b200.core import config_spec
+    from paper_2103_08825_b200.plan import _problem as mk
+    prob, keep = mk(config_spec(key), dims, "f64", arith, k, "auto", 0)
+    prob._keep = keep
+    return prob
+
+
+@pytest.mark.parametrize("key,dims,arith,want", [
+    ("c1", (1 << 20,), "fma", 64), ("c2", (1 << 26,), "fma", 32), ("c2", (1 << 20,), "exact", 16),
+    ("c3a", (512, 512), "fma", 32), ("c3b", (512, 512), "fma", 4), ("c4", (64, 64, 64), "fma", 2),
+    ("c5", (64, 64, 64), "exact", 2),
+])
+def test_problem_k_resolves_without_a_device(lib, key, dims, arith, want):
+    k = ctypes.c_int32()
+    prob = _config_problem(key, dims, arith)
+    assert lib.sb_problem_k(ctypes.byref(prob), ctypes.byref(k)) == _abi.SB_OK
+    assert k.value == want
+
+
+def test_multi_create_fails_loudly_without_devices(lib):
+    if lib.sb_device_count() > 0:
+        pytest.skip("a device is visible")
+    h = ctypes.c_void_p()
+    prob = _config_problem("c5", (64, 64, 64), "fma")
+    rc = lib.sb_multi_create(ctypes.byref(h), ctypes.byref(prob), 2, None)
+    assert rc in (_abi.SB_ERR_ARG, _abi.SB_ERR_CUDA) and not h.value
