@@ -351,8 +351,9 @@ def run_gpu_arm(args):
     upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
     download = lambda: plan.download(host_out.numpy())       # noqa: E731
 
-    # one sweep = T steps; at N=1 every launch of the sweep is bracketed by
-    # CUDA events on the plan stream (per-launch durations of the timed region)
+    # one sweep = T steps; at N=1 a CUDA event on the plan stream precedes every
+    # launch of the timed region (one more closes it): consecutive events
+    # bracket each launch, so the per-launch durations are measured live
     n_full, tail = divmod(T, k)
     chunks = [k] * n_full + ([tail] if tail else [])
 
@@ -360,7 +361,6 @@ def run_gpu_arm(args):
         for j, kk in enumerate(chunks):
             evs[j].record(stream)
             plan.launch(kk)
-        evs[len(chunks)].record(stream)
 
     def barrier():
         if dist is not None:
@@ -376,7 +376,7 @@ def run_gpu_arm(args):
             plan.launch(T)
     barrier()
 
-    launch_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(chunks) + 1)]
+    launch_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(chunks))]
                   for _ in range(args.steps)] if world == 1 else None
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -406,7 +406,8 @@ def run_gpu_arm(args):
     # event-timed full-depth launches of the timed region; N>1: the step time
     # spread over the launches (edge/interior/exchange overlap inside).
     if world == 1:
-        full = [launch_evs[i][j].elapsed_time(launch_evs[i][j + 1])
+        flat = [e for evs in launch_evs for e in evs] + [ev1]
+        full = [flat[i * len(chunks) + j].elapsed_time(flat[i * len(chunks) + j + 1])
                 for i in range(args.steps) for j in range(n_full)]
         launch_ms = statistics.mean(full)
         launch_src = (f"CUDA events around each of the {len(full)} full-depth (k={k}) launches of the timed "
