@@ -165,7 +165,7 @@ class ClockSampler:
             if len(parts) < 7:
                 continue
             try:
-                parsed.append((t, float(parts[0]), float(parts[1]), parts[3:7]))
+                parsed.append((t, float(parts[0]), float(parts[1]), parts[3:7], float(parts[2])))
             except ValueError:
                 continue
         if not parsed:
@@ -178,7 +178,8 @@ class ClockSampler:
             window = "nearest to a timed region shorter than the sampling period"
         reasons = sorted({nm for p in inside for nm, v in zip(self.NAMES, p[3]) if v.lower() == "active"})
         return {"sm_mhz": statistics.median(p[1] for p in inside), "sm_max_mhz": inside[-1][2],
-                "reasons": reasons, "samples": len(inside), "window": window}
+                "reasons": reasons, "samples": len(inside), "window": window,
+                "power_w_median": statistics.median(p[4] for p in inside)}
 
 
 def dist_env():
@@ -213,16 +214,37 @@ def cpu_reference_rate(spec, dims, sample_steps=None, budget_s=10.0):
     return rate, threads, f"{sample_steps} steps of the full {'x'.join(map(str, dims))} grid (same spec)"
 
 
-def numpy_reference_rate(spec, n, steps=2):
-    """The reference's own arithmetic as numpy restates it (1 core; 1D lines)."""
-    from oracle import np_oracle
-    from paper_2103_08825_b200.core import canonical
-    offs, ws = canonical(spec)
-    box = np.random.default_rng(12345).random(n + 2 * spec.r)
-    t0 = time.perf_counter()
-    np_oracle.sweep(box, spec.r, offs, ws, steps)
-    dt = time.perf_counter() - t0
-    return n * steps / dt / 1e9
+def reference_numpy_rate(spec, dims, budget_s=6.0):
+    """The reference's own code: ``stencilbench.kernels.scalar_step`` (numpy,
+    one core) from the installed reference (baseline/_ref), one step over a
+    slab of the workload grid sized to ~budget_s.  None when not installed."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "stencilbench")) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        from stencilbench import core as sc
+        from stencilbench import kernels as sk
+    except ImportError:
+        return None
+    rspec = sc.StencilSpec(spec.name, spec.d, spec.r, spec.shape, dict(spec.weights))
+    plane = int(np.prod(dims[1:])) if len(dims) > 1 else 1
+
+    def one(n0):
+        sub = (n0,) + tuple(dims[1:])
+        a = sc.alloc_grid(rspec, sub, sc.Layout.NATURAL, 4)
+        a.set_interior(np.random.default_rng(1).random(sub))
+        b = sc.alloc_like(a)
+        t0 = time.perf_counter()
+        sk.scalar_step(a, b, rspec)
+        return n0 * plane / (time.perf_counter() - t0), sub
+
+    n0 = max(1, min(dims[0], (1 << 16) // plane if plane < (1 << 16) else 1))
+    rate, sub = one(n0)
+    n0 = int(max(1, min(dims[0], budget_s * rate / plane)))
+    rate, sub = one(n0)
+    return {"value": rate / 1e9, "unit": "GStencil/s", "cores": 1, "kind": "reference",
+            "sample": f"one stencilbench.kernels.scalar_step (numpy) over {'x'.join(map(str, sub))} "
+                      f"of the workload grid, from the installed reference (baseline/_ref)"}
 
 
 def run_reference_arm(args):
@@ -265,6 +287,10 @@ def run_reference_arm(args):
         "e2e": {"value": value, "unit": "GStencil/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    try:
+        line["reference_numpy"] = reference_numpy_rate(spec, dims)
+    except MemoryError:
+        pass
     print(json.dumps(line), flush=True)
 
 
@@ -282,6 +308,8 @@ def kernel_label(spec, wl, k, arith):
         return f"fused2d_kernel (K={k})"
     if spec.shape == "star" and arith == "fma" and k == 2 and wl.get("dtype", "f64") == "f64":
         return "compose3d_kernel (two steps as one 25-point pass)"
+    if spec.shape == "box" and k == 2:
+        return "box3d_kernel (64xTY output tiles, ring-only level-1 recompute)"
     return f"fused3d_kernel (K={k})"
 
 
@@ -383,12 +411,19 @@ def run_gpu_arm(args):
     kernels_before = plan.kernel_count()
     barrier()
     clocks.mark_start()
+    # a sweep that is ONE launch (C1: ~10 us) is enqueued natively, K back-to-back
+    # sweeps with an event around each (sb_launch_repeat): a Python loop with
+    # per-launch events would bound it by the interpreter, not the GPU
+    native_repeat = world == 1 and len(chunks) == 1
     ev0.record(stream)
-    for i in range(args.steps):
-        if world > 1:
-            runner.run(T)
-        else:
-            sweep_events(launch_evs[i])
+    if native_repeat:
+        plan.launch_repeat(T, args.steps)
+    else:
+        for i in range(args.steps):
+            if world > 1:
+                runner.run(T)
+            else:
+                sweep_events(launch_evs[i])
     ev1.record(stream)
     barrier()
     clocks.mark_end()
@@ -405,7 +440,16 @@ def run_gpu_arm(args):
     # Dominant kernel: the main launch of k fused steps.  N=1: mean of the
     # event-timed full-depth launches of the timed region; N>1: the step time
     # spread over the launches (edge/interior/exchange overlap inside).
-    if world == 1:
+    if native_repeat:
+        # the timed region is nothing but the dominant kernel, back to back (programmatic
+        # dependent launch between sweeps): its mean duration is the region / launches
+        # (events between launches would add ~2.5 us of device time to each ~10 us sweep)
+        total = plan.repeat_times()[0]
+        launch_ms = total / args.steps
+        launch_src = (f"CUDA events around the {args.steps} back-to-back launches of the timed region (one k={k} "
+                      f"launch per sweep, nothing else on the stream; sb_launch_repeat)")
+        share = total / ms
+    elif world == 1:
         flat = [e for evs in launch_evs for e in evs] + [ev1]
         full = [flat[i * len(chunks) + j].elapsed_time(flat[i * len(chunks) + j + 1])
                 for i in range(args.steps) for j in range(n_full)]
@@ -585,11 +629,10 @@ def run_gpu_arm(args):
                "sample": sample + "; oracle/oracle.c (bit-exact restatement of "
                                   "stencilbench scalar_step), OpenMP"
                                   + (", fp64 (the reference is fp64-only)" if dtype == "f32" else "")}
-        if len(dims) == 1:
-            try:
-                cpu["numpy_1core_gstencil"] = numpy_reference_rate(spec, n_local)
-            except MemoryError:
-                pass
+        try:
+            cpu["reference_numpy"] = reference_numpy_rate(spec, dims)
+        except MemoryError:
+            pass
 
     if rank == 0:
         grid_bytes = int(np.prod([d + 2 * spec.r for d in plan.dims])) * es

@@ -133,6 +133,16 @@ int sb_run(sb_plan *plan, int64_t steps, sb_timing *timing);
 /* Same, asynchronously on the plan stream (no host sync, no timing). */
 int sb_launch(sb_plan *plan, int64_t steps);
 
+/* `repeats` back-to-back sweeps of `steps` steps (sb_launch each), enqueued
+ * from native code: short sweeps (C1: one ~10 us launch) are not bound by the
+ * caller's per-call overhead.  Asynchronous.  Events are recorded before the
+ * first sweep and after the last, and with per_sweep_events != 0 also
+ * between sweeps (each costs ~2.5 us of device time between 10 us launches).
+ * sb_repeat_times waits and writes up to `cap` durations (ms): one per sweep,
+ * or the whole run; returns how many it recorded. */
+int sb_launch_repeat(sb_plan *plan, int64_t steps, int32_t repeats, int32_t per_sweep_events);
+int sb_repeat_times(sb_plan *plan, float *sweep_ms, int32_t cap);
+
 /* One fused launch of `steps` levels that writes only the slowest-axis
  * interior positions [lo, hi) of the other buffer, reading the current one.
  * A step is split into several range launches (e.g. the slab's edge planes

@@ -26,7 +26,7 @@ EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
            "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
            "sb_multi_create", "sb_multi_destroy", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
-           "sb_multi_info", "sb_multi_slab", "sb_problem_k")
+           "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times")
 
 
 class SbProblem(ctypes.Structure):
@@ -103,6 +103,8 @@ def load():
     lib.sb_multi_slab.argtypes = [P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
                                   ctypes.POINTER(ctypes.c_int32)]
     lib.sb_problem_k.argtypes = [ctypes.POINTER(SbProblem), ctypes.POINTER(ctypes.c_int32)]
+    lib.sb_launch_repeat.argtypes = [P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
+    lib.sb_repeat_times.argtypes = [P, ctypes.POINTER(ctypes.c_float), ctypes.c_int32]
     lib.sb_last_error.restype = ctypes.c_char_p
     lib.sb_last_error.argtypes = []
     lib.sb_abi_version.restype = ctypes.c_int
@@ -112,7 +114,7 @@ def load():
                  "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
                  "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
                  "sb_multi_create", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
-                 "sb_multi_info", "sb_multi_slab", "sb_problem_k"):
+                 "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -133,6 +133,11 @@ edge_window_kernel(const EdgeWindowParams<T, R> P) {
 template <typename T, int HALF, int R = 0>   // HALF = R*K
 __global__ void __launch_bounds__(C1_WARPS * 32)
 compose1d_kernel(const Compose1DParams<T> P, const EdgeWindowParams<T, (R > 0 ? R : 1)> EP = {}, int nedge = 0) {
+    // Programmatic dependent launch: this grid may be scheduled while the previous
+    // launch on the stream (the previous sweep step, which wrote our input) drains;
+    // wait here for it to complete before touching its output or the tile queue.
+    // (A no-op when launched without the attribute.)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (R > 0) {
         if ((int)blockIdx.x < nedge) {
             if (threadIdx.x < 32) edge_window_body<T, R, HALF / R, true>(EP, blockIdx.x, threadIdx.x);

@@ -221,9 +221,22 @@ int launch_compose1d_k(sb_plan* P, const T* src, T* dst) {
                                          sb::compose1d_smem_bytes<T, HALF>()));
             attr_set.fetch_or(1ull << (P->device & 63));
         }
-        ck<<<(unsigned)(main_blocks + sc->nedge), sb::C1_WARPS * 32, sb::compose1d_smem_bytes<T, HALF>(), P->stream>>>(
-            cp, ep, sc->nedge);
-        SB_CUDA(cudaGetLastError());
+        // programmatic dependent launch: CTA scheduling and the launch latency of this
+        // step overlap the previous step's tail (the kernel waits on griddepcontrol
+        // before reading); short sweeps (C1: one ~10 us launch per step) gain most
+        static const int pdl = (int)env_double("SB200_PDL", 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(main_blocks + sc->nedge));
+        cfg.blockDim = dim3(sb::C1_WARPS * 32);
+        cfg.dynamicSmemBytes = sb::compose1d_smem_bytes<T, HALF>();
+        cfg.stream = P->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        const int nedge = sc->nedge;
+        SB_CUDA(cudaLaunchKernelEx(&cfg, ck, cp, ep, nedge));
         return SB_OK;
     }
     if (cp.ntiles > 0) {

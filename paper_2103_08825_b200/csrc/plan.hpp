@@ -87,6 +87,8 @@ struct sb_plan {
     unsigned int* d_counter = nullptr;  // work queue of the persistent kernels
     std::vector<sbh::Sched1D> sched1d;
     std::vector<SweepGraph> graphs;       // captured sweeps (see run_graphed)
+    std::vector<cudaEvent_t> rep_ev;      // sb_launch_repeat: event before each sweep (+1 after)
+    int rep_n = 0;                        // sweeps recorded by the last sb_launch_repeat
     CUtensorMap tmap[8][2];                // TMA descriptors [geometry][buffer] (3D; 2, 3: composed; 4-6: box3d)
     bool tmap_ok[8] = {false, false, false, false, false, false, false, false};
     void* tmp = nullptr;                   // scratch grid of the separable composed 2D path

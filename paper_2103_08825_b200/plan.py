@@ -193,6 +193,20 @@ class Plan:
     def launch(self, steps: int) -> None:
         _abi.check(self._lib.sb_launch(self._h, int(steps)))
 
+    def launch_repeat(self, steps: int, repeats: int, per_sweep_events: bool = False) -> None:
+        """``repeats`` back-to-back sweeps of ``steps`` steps enqueued natively
+        (see :meth:`repeat_times`).  Asynchronous."""
+        _abi.check(self._lib.sb_launch_repeat(self._h, int(steps), int(repeats), 1 if per_sweep_events else 0))
+
+    def repeat_times(self) -> list[float]:
+        """Durations (ms) of the last :meth:`launch_repeat` (waits for it): one
+        per sweep with per-sweep events, else one for the whole run."""
+        buf = (ctypes.c_float * 65536)()
+        n = self._lib.sb_repeat_times(self._h, buf, 65536)
+        if n < 0:
+            _abi.check(n)
+        return [float(buf[i]) for i in range(min(n, 65536))]
+
     def launch_range(self, steps: int, lo: int, hi: int, finish: bool) -> None:
         """One fused launch writing only slowest-axis interior positions [lo, hi);
         ``finish`` completes the step (swaps buffers).  Asynchronous."""
