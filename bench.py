@@ -204,9 +204,12 @@ def cpu_reference_rate(spec, dims, sample_steps=None, budget_s=10.0):
     box = seeded_host_box(dims, spec.r)
     t0 = time.perf_counter()
     c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
-    one = time.perf_counter() - t0
+    t1 = time.perf_counter()
+    c_oracle.sweep(box, spec.r, offs, ws, 3, threads=threads, inplace=True)
+    t3 = time.perf_counter()
+    one = max((t3 - t1) - (t1 - t0), 1e-6) / 2       # marginal step (a call also copies the grid)
     if sample_steps is None:
-        sample_steps = int(max(1, min(1000, budget_s / max(one, 1e-6))))
+        sample_steps = int(max(2, min(1000, budget_s / one)))
     t0 = time.perf_counter()
     c_oracle.sweep(box, spec.r, offs, ws, sample_steps, threads=threads, inplace=True)
     dt = time.perf_counter() - t0
@@ -261,10 +264,14 @@ def run_reference_arm(args):
     offs, ws = canonical(spec)
     threads = c_oracle.max_threads()
     box = seeded_host_box(dims, spec.r)
+    # marginal cost of a step (a call also allocates and copies the partner grid)
     t0 = time.perf_counter()
     c_oracle.sweep(box, spec.r, offs, ws, 1, threads=threads, inplace=True)
-    one = time.perf_counter() - t0
-    per_step = int(max(1, min(wl["T"], 8.0 / max(one, 1e-6))))   # ~8 s per bench step
+    t1 = time.perf_counter()
+    c_oracle.sweep(box, spec.r, offs, ws, 3, threads=threads, inplace=True)
+    t3 = time.perf_counter()
+    one = max((t3 - t1) - (t1 - t0), 1e-6) / 2
+    per_step = int(max(2, min(wl["T"], 8.0 / one)))   # ~8 s per bench step
     for _ in range(args.warmup):
         c_oracle.sweep(box, spec.r, offs, ws, max(1, per_step // 4), threads=threads, inplace=True)
     times = []
