@@ -383,7 +383,9 @@ def run_gpu_arm(args):
     host_in = torch.empty(plan.shape, dtype=torch_dtype, pin_memory=True)
     host_in.numpy()[...] = rng.random(plan.shape)
     host_out = torch.empty_like(host_in, pin_memory=True)
-    upload = lambda: plan.upload(host_in.numpy())            # noqa: E731
+    # slab runs upload through the runner (it re-exchanges the uploaded ghost planes)
+    upload = ((lambda: runner.upload(host_in.numpy())) if world > 1      # noqa: E731
+              else (lambda: plan.upload(host_in.numpy())))
     download = lambda: plan.download(host_out.numpy())       # noqa: E731
 
     # one sweep = T steps; at N=1 a CUDA event on the plan stream precedes every

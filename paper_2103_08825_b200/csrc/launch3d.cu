@@ -371,6 +371,7 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     static const int skew = (int)env_double("SB200_B3_SKEW", 0);
     if (skew && nw == 4) return launch_box3d<T, FMA, 4, 4, false, true>(P, src_idx);
     if (skew && nw == 8) return launch_box3d<T, FMA, 8, 2, false, true>(P, src_idx);
+    if (nw == 3 && minb == 4) return launch_box3d<T, FMA, 3, 4>(P, src_idx);
     if (nw == 3) return launch_box3d<T, FMA, 3, 5>(P, src_idx);
     if (nw == 4 && minb == 3) return launch_box3d<T, FMA, 4, 3>(P, src_idx);
     if (nw == 4) return launch_box3d<T, FMA, 4, 4>(P, src_idx);
