@@ -25,6 +25,7 @@
 // slab (ghost) sides along y compute normally.
 #pragma once
 #include <climits>
+#include <type_traits>
 #include "common.cuh"
 #include "fused1d.cuh"   // cp.async helpers, Vec16
 
@@ -90,11 +91,14 @@ __device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, bool
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 4 : 0));
 }
 
+// Fold an arriving level-(l-1) row a into three pending-row sets: Pm = row
+// a-1 (its dy=+1 terms complete it), P0 = row a (dy=0), nx = row a+1 (dy=-1,
+// started here).  The caller rotates the roles of the three sets from row to
+// row by renaming (the row loop is unrolled x3), so no register moves.
 template <typename T, bool BOX, bool FMA, bool SEP = false>
-__device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX], T (&P0)[F2_VX], T (&done)[F2_VX],
-                                        const T* w, const T* sa = nullptr, const T* sb = nullptr) {
+__device__ __forceinline__ void f2_push3(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX], T (&P0)[F2_VX], T (&nx)[F2_VX],
+                                         const T* w, const T* sa = nullptr, const T* sb = nullptr) {
     // u[0] = column -1, u[1..VX] = own columns, u[VX+1] = column VX
-    T nx[F2_VX];
     if (SEP) {
         // rank-1 box weights w[dy][dx] = sa[dy] * sb[dx] (FMA mode only): one horizontal
         // 3-tap pass, then the vertical push -- 6 instead of 9 FMAs per point and level
@@ -131,12 +135,6 @@ __device__ __forceinline__ void f2_push(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX],
         for (int j = 0; j < F2_VX; j++) P0[j] = acc_term<T, FMA>(P0[j], w[4], u[j + 1]);   // (0,0)
 #pragma unroll
         for (int j = 0; j < F2_VX; j++) P0[j] = acc_term<T, FMA>(P0[j], w[5], u[j + 2]);   // (0,1)
-    }
-#pragma unroll
-    for (int j = 0; j < F2_VX; j++) {
-        done[j] = Pm[j];
-        Pm[j] = P0[j];
-        P0[j] = nx[j];
     }
 }
 
@@ -228,13 +226,16 @@ fused2d_kernel(const Fused2DParams<T> P) {
         for (int t = 0; t < F2_DEPTH - 1; t++) stage();
         int slot_t = 0;                                 // ring slot of row t
 
-        T Pm[K][F2_VX], P0[K][F2_VX];
+        T A[K][3][F2_VX];   // per level: pending-row sets, roles rotating with t (mod 3)
 #pragma unroll
         for (int l = 0; l < K; l++)
 #pragma unroll
-            for (int j = 0; j < F2_VX; j++) Pm[l][j] = P0[l][j] = T(0);
+            for (int q = 0; q < 3; q++)
+#pragma unroll
+                for (int j = 0; j < F2_VX; j++) A[l][q][j] = T(0);
 
-        for (int t = 0; t < M; t++) {
+        auto row_step = [&](int t, auto rot) {
+            constexpr int IC = decltype(rot)::value, IK = (IC + 1) % 3, IS = (IC + 2) % 3;
             cp_async_wait<F2_DEPTH - 2>();
             __syncwarp();
             const T* row = ring + slot_t * F2_ROWW;
@@ -258,8 +259,8 @@ fused2d_kernel(const Fused2DParams<T> P) {
                 u[F2_VX + 1] = (l == 1 && lane == 31) ? edge : right;
 #pragma unroll
                 for (int j = 0; j < F2_VX; j++) u[j + 1] = v[j];
-                T done[F2_VX];
-                f2_push<T, BOX, FMA, SEP>(u, Pm[l - 1], P0[l - 1], done, P.w, P.sa, P.sb);
+                f2_push3<T, BOX, FMA, SEP>(u, A[l - 1][IC], A[l - 1][IK], A[l - 1][IS], P.w, P.sa, P.sb);
+                T (&done)[F2_VX] = A[l - 1][IC];        // completed: row a0 - l of level l
                 const int yc = a0 - l;                      // completed level-l row
                 const bool y_out = yc < ylo || yc >= yhi;
                 if (!plain && y_out) {                      // (warp-uniform) physical y-halo row
@@ -300,6 +301,26 @@ fused2d_kernel(const Fused2DParams<T> P) {
                 }
             }
             slot_t = slot_t + 1 == RING ? 0 : slot_t + 1;
+        };
+        if constexpr (K <= 4) {
+            // roles renamed by unrolling x3 (no moves): C3b k=4 1041-1047 vs 1025 GStencil/s
+            for (int t = 0; t < M; t += 3) {
+                row_step(t, std::integral_constant<int, 0>());
+                if (t + 1 < M) row_step(t + 1, std::integral_constant<int, 1>());
+                if (t + 2 < M) row_step(t + 2, std::integral_constant<int, 2>());
+            }
+        } else {
+            // k = 8: the x3 body needs 254 registers (769 vs 968 GStencil/s); rotate by moves
+            for (int t = 0; t < M; t++) {
+                row_step(t, std::integral_constant<int, 0>());
+#pragma unroll
+                for (int l = 0; l < K; l++)
+#pragma unroll
+                    for (int j = 0; j < F2_VX; j++) {
+                        A[l][0][j] = A[l][1][j];
+                        A[l][1][j] = A[l][2][j];
+                    }
+            }
         }
         cp_async_wait<0>();
         __syncwarp();
