@@ -344,6 +344,7 @@ def run_gpu_arm(args):
     dist = None
     if world > 1:
         os.environ.setdefault("NCCL_DEBUG", "INFO")           # lets the driver count communicator ranks
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # stdout carries only the JSON line
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl")

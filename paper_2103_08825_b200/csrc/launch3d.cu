@@ -366,6 +366,7 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     // measured 630 vs 600-635 GStencil/s on C5 fp32
     static const int u3 = (int)env_double("SB200_B3_U3", 1);
     if constexpr (sizeof(T) == 4 && FMA) {
+        if (u3 && nw == 4 && minb == 5) return launch_box3d<T, FMA, 4, 5, true>(P, src_idx);
         if (u3 && nw == 4) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
     }
     static const int skew = (int)env_double("SB200_B3_SKEW", 0);
