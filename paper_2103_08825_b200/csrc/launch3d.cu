@@ -368,6 +368,7 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     if constexpr (sizeof(T) == 4 && FMA) {
         if (u3 && nw == 4 && minb == 5) return launch_box3d<T, FMA, 4, 5, true>(P, src_idx);
         if (u3 && nw == 4) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
+        if (u3 && nw == 8) return launch_box3d<T, FMA, 8, 2, true>(P, src_idx);
     }
     static const int skew = (int)env_double("SB200_B3_SKEW", 0);
     if (skew && nw == 4) return launch_box3d<T, FMA, 4, 4, false, true>(P, src_idx);

@@ -2,7 +2,7 @@
 # launch lists and one `ncu --set full` capture of each workload's dominant
 # kernel (summarised on the box: raw metrics CSV + stall/opcode summary).
 set -u
-O=gpurun_out/r02
+O=${EVID_OUT:-gpurun_out/r02}
 mkdir -p $O/wl $O/ncu
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,power.limit --format=csv > $O/smi.txt
 timeout 400 python bench.py --steps 10 --warmup 3 --verify > $O/bench_default.json 2> $O/bench_default.err
@@ -28,7 +28,7 @@ cap c5_box3d c5 box3d 10 ""
 cap c5f32_box3d c5f32 box3d 10 ""
 cap c4_compose3d c4 compose3d_kernel 10 ""
 cap c2_compose1d c2 compose1d 10 ""
-cap c1_compose1d c1 compose1d 3 ""
+cap c1_compose1d c1 compose1d 1 ""
 cap c3a_sep_vpass c3a sep_vpass 5 ""
 cap c3a_sep_hpass c3a sep_hpass 5 ""
 cap c3b_fused2d c3b fused2d 20 ""
