@@ -81,9 +81,7 @@ struct Box3DParams {
     int phys_lo, phys_hi;
     int tiles_x, tiles_y, nseg, lz, items, total_ctas;
     int z0, z1;              // output planes [z0, z1) of this launch (range launches)
-    unsigned int* counter;   // [0] next item (queue 0), [2] queue 1, [1] retired CTAs
-    int split;               // 0: one queue; 1/2: per half of the tile columns by SM id (< n/2 / parity)
-    int num_sms, q_items[2];
+    unsigned int* counter;   // [0] next item, [1] retired CTAs
     T w[27];                 // w[(dz+1)*9 + (dy+1)*3 + (dx+1)]
     unsigned long long wpp[27];   // fp32: (w, w) pairs for the packed FFMA2 push
 };
@@ -227,7 +225,7 @@ __device__ __forceinline__ void b3_st2(T* p, const B3Acc<T, PAIR, RPT>& A, int i
     else *reinterpret_cast<float2*>(p) = make_float2(A.v[i][0], A.v[i][1]);
 }
 
-template <typename T, bool FMA, int NW, int MINB, bool U3, bool SKEW>
+template <typename T, bool FMA, int NW, int MINB, bool U3>
 __global__ void __launch_bounds__(32 * NW, MINB)
 box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
     using G = B3Geo<T, NW>;
@@ -241,17 +239,12 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
     T* s0 = reinterpret_cast<T*>(smem_b3);      // B3_NS0 level-0 slots
     T* s1 = s0 + B3_NS0 * PLANE;                 // two level-1 planes (+ two shifted copies)
     __shared__ uint64_t bar[B3_NS0];
-    __shared__ uint64_t barF[2], barE[2];   // SKEW: level-1 buffer full / empty
     __shared__ unsigned s_item;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         for (int i = 0; i < B3_NS0; i++) mbar_init(&bar[i], 1);
-        for (int i = 0; i < 2; i++) {
-            mbar_init(&barF[i], 32 * NW);
-            mbar_init(&barE[i], 32 * NW);
-        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
     }
@@ -275,44 +268,14 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
     // TMA ring position of the next arrival (CTA lifetime): slot and mbarrier parity
     int gslot = 0;
     unsigned gphase = 0;
-    unsigned gw = 0;   // SKEW: level-1 planes written so far
     for (;;) {
-        // work queues: one, or (split) one per half of the tile columns, each served
-        // first by the CTAs of one half of the SMs (same die: tiles that share halo
-        // rows/columns then meet in the same L2) and then stolen by the others
-        if (tid == 0) {
-            unsigned it = 0xffffffffu;
-            if (P.split) {
-                unsigned smid;
-                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-                const int own = P.split == 1 ? ((int)smid >= P.num_sms / 2) : (int)(smid & 1);
-                for (int k = 0; k < 2 && it == 0xffffffffu; k++) {
-                    const int q = own ^ k;
-                    const unsigned i = atomicAdd(&P.counter[q ? 2 : 0], 1u);
-                    if (i < (unsigned)P.q_items[q]) it = ((unsigned)q << 31) | i;
-                }
-            } else {
-                const unsigned i = atomicAdd(&P.counter[0], 1u);
-                if (i < (unsigned)P.items) it = i;
-            }
-            s_item = it;
-        }
+        if (tid == 0) s_item = atomicAdd(&P.counter[0], 1u);
         __syncthreads();
         const unsigned item = s_item;
-        if (item == 0xffffffffu) break;
-        int tix, tiy, seg;
-        if (P.split) {
-            const int q = item >> 31;
-            const unsigned i = item & 0x7fffffffu;
-            const int wq = q ? P.tiles_x - P.tiles_x / 2 : P.tiles_x / 2;
-            tix = (q ? P.tiles_x / 2 : 0) + (int)(i % wq);
-            tiy = (int)((i / wq) % P.tiles_y);
-            seg = (int)(i / (wq * P.tiles_y));
-        } else {
-            tix = item % P.tiles_x;
-            tiy = (item / P.tiles_x) % P.tiles_y;
-            seg = item / (P.tiles_x * P.tiles_y);
-        }
+        if (item >= (unsigned)P.items) break;
+        const int tix = item % P.tiles_x;
+        const int tiy = (item / P.tiles_x) % P.tiles_y;
+        const int seg = item / (P.tiles_x * P.tiles_y);
         const int x0 = tix * 64, y0 = tiy * TY;
 
         // level-1 points: main (x0-1+2*lane+j, y0+4*warp+i), ring job (x0+rj_dx+j, y0+rj_dy)
@@ -456,46 +419,7 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
             level2(t, rot, l1);
         };
 
-        if constexpr (SKEW) {
-            // Skewed levels without a CTA barrier: iteration t runs level 1 of arrival t
-            // and level 2 of arrival t-1.  Level-1 planes alternate between two buffers
-            // guarded by mbarriers: "full" (every thread stored its part; level 2 waits on
-            // it one iteration after the stores, when it has long completed) and "empty"
-            // (every thread finished its level-2 reads; level 1 waits on it before
-            // overwriting the buffer two planes later).  Warps drift by up to an
-            // iteration instead of meeting at a barrier twice per plane.
-            int rslot = slot;   // ring slot of the previous arrival (refilled once its readers are done)
-            for (int t = 0; t <= M; t++) {
-                if (t < M) {
-                    const unsigned w = gw + t;   // CTA-lifetime index of this level-1 plane
-                    T* l1 = s1 + (w & 1) * PLANE;
-                    const int cur = slot;
-                    auto ic = level1(t, std::integral_constant<int, 0>(), l1);
-                    if (w >= 2) mbar_wait(&barE[w & 1], ((w - 2) >> 1) & 1);
-                    store_l1(ic, l1);
-                    mbar_arrive(&barF[w & 1]);
-                    next_slot();
-                    A[0] = A[1]; A[1] = A[2];
-                    R[0] = R[1]; R[1] = R[2];
-                    if (t >= 1) {
-                        const unsigned r = w - 1;
-                        mbar_wait(&barF[r & 1], (r >> 1) & 1);
-                        if (tid == 0 && t - 1 + B3_NS0 < M) issue(t - 1 + B3_NS0, rslot);
-                        level2(t - 1, std::integral_constant<int, 0>(), s1 + (r & 1) * PLANE);
-                        mbar_arrive(&barE[r & 1]);
-                        B[0] = B[1]; B[1] = B[2];
-                    }
-                    rslot = cur;
-                } else {
-                    const unsigned r = gw + t - 1;
-                    mbar_wait(&barF[r & 1], (r >> 1) & 1);
-                    level2(t - 1, std::integral_constant<int, 0>(), s1 + (r & 1) * PLANE);
-                    mbar_arrive(&barE[r & 1]);
-                    B[0] = B[1]; B[1] = B[2];
-                }
-            }
-            gw += M;
-        } else if constexpr (UNROLL3) {
+        if constexpr (UNROLL3) {
             // accumulator roles rotate by renaming: no register moves (fp32: they would
             // compete with the FFMA2s for the FMA pipe)
             for (int t = 0; t < M; t += 3) {
@@ -521,7 +445,6 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
         const unsigned retired = atomicAdd(&P.counter[1], 1u);
         if (retired == (unsigned)P.total_ctas - 1) {
             atomicExch(&P.counter[0], 0u);
-            atomicExch(&P.counter[2], 0u);
             atomicExch(&P.counter[1], 0u);
         }
     }

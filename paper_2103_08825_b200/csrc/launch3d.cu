@@ -294,7 +294,7 @@ int launch_compose3d_t(sb_plan* P, int src_idx) {
 // ---- 27-point box, k = 2: output tiles of exactly 64 x TY, ring-only
 // level-1 recompute (box3d.cuh)
 
-template <typename T, bool FMA, int NW, int MINB, bool U3 = false, bool SKEW = false>
+template <typename T, bool FMA, int NW, int MINB, bool U3 = false>
 int launch_box3d(sb_plan* P, int src_idx) {
     using G = sb::B3Geo<T, NW>;
     constexpr int GEO = NW == 4 ? 4 : (NW == 8 ? 5 : 6);   // tensor-map slot of this box geometry
@@ -302,7 +302,7 @@ int launch_box3d(sb_plan* P, int src_idx) {
         const int rc = make_tensor_maps_impl(P, GEO, G::PH, G::PW);
         if (rc != SB_OK) return rc;
     }
-    auto kern = sb::box3d_kernel<T, FMA, NW, MINB, U3, SKEW>;
+    auto kern = sb::box3d_kernel<T, FMA, NW, MINB, U3>;
     SB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM));
     int occ = 0;
     SB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, G::THREADS, G::SMEM));
@@ -336,11 +336,6 @@ int launch_box3d(sb_plan* P, int src_idx) {
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
-    static const int split = (int)env_double("SB200_B3_SPLIT", 0);
-    prm.split = prm.tiles_x >= 2 ? split : 0;
-    prm.num_sms = P->num_sms;
-    prm.q_items[0] = (prm.tiles_x / 2) * prm.tiles_y * prm.nseg;
-    prm.q_items[1] = (prm.tiles_x - prm.tiles_x / 2) * prm.tiles_y * prm.nseg;
     for (int i = 0; i < 27; i++) prm.w[i] = T(0);
     for (int i = 0; i < P->nw; i++) {
         const int* o = &P->offsets[3 * i];
@@ -360,24 +355,22 @@ int launch_box3d(sb_plan* P, int src_idx) {
 
 template <typename T, bool FMA>
 int launch_box3d_t(sb_plan* P, int src_idx) {
+    // measured (C5, T=100): NW=4 (64 x 16 tiles, 4 CTAs/SM) 402-413 GStencil/s fp64,
+    // NW=8 (64 x 32, 2/SM) 403-410, 3 CTAs/SM without a register cap 399-409;
+    // rejected: 96-thread CTAs (366-377), a skewed pipeline on mbarriers (390-402),
+    // per-die work queues (402), a warp-specialised level split (335)
     static const int nw = (int)env_double("SB200_B3_NW", 4);
     static const int minb = (int)env_double("SB200_B3_MINB", 0);
     // fp32: the 3x-unrolled loop (roles renamed, no accumulator moves on the FMA pipe)
     // measured 630 vs 600-635 GStencil/s on C5 fp32
     static const int u3 = (int)env_double("SB200_B3_U3", 1);
     if constexpr (sizeof(T) == 4 && FMA) {
-        if (u3 && nw == 4 && minb == 5) return launch_box3d<T, FMA, 4, 5, true>(P, src_idx);
-        if (u3 && nw == 4) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
         if (u3 && nw == 8) return launch_box3d<T, FMA, 8, 2, true>(P, src_idx);
+        if (u3) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
     }
-    static const int skew = (int)env_double("SB200_B3_SKEW", 0);
-    if (skew && nw == 4) return launch_box3d<T, FMA, 4, 4, false, true>(P, src_idx);
-    if (skew && nw == 8) return launch_box3d<T, FMA, 8, 2, false, true>(P, src_idx);
-    if (nw == 3 && minb == 4) return launch_box3d<T, FMA, 3, 4>(P, src_idx);
-    if (nw == 3) return launch_box3d<T, FMA, 3, 5>(P, src_idx);
-    if (nw == 4 && minb == 3) return launch_box3d<T, FMA, 4, 3>(P, src_idx);
-    if (nw == 4) return launch_box3d<T, FMA, 4, 4>(P, src_idx);
-    return launch_box3d<T, FMA, 8, 2>(P, src_idx);
+    if (nw == 8) return launch_box3d<T, FMA, 8, 2>(P, src_idx);
+    if (minb == 3) return launch_box3d<T, FMA, 4, 3>(P, src_idx);
+    return launch_box3d<T, FMA, 4, 4>(P, src_idx);
 }
 
 bool box3d_ok(const sb_plan* P, int k) {
