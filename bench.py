@@ -346,8 +346,12 @@ def run_gpu_arm(args):
         os.environ.setdefault("NCCL_DEBUG", "INFO")           # lets the driver count communicator ranks
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")   # stdout carries only the JSON line
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # SB200_SHARE_GPU=1 (TEST mode, tools/share_gpu_bench.sh): every rank on cuda:0 over
+        # gloo, the slab exchange staged through the host -- checks this N>1 code path on a
+        # one-GPU box; its numbers are not scaling measurements
+        share_gpu = bool(os.environ.get("SB200_SHARE_GPU"))
+        torch.cuda.set_device(0 if share_gpu else local)
+        dist.init_process_group("gloo" if share_gpu else "nccl")
     else:
         torch.cuda.set_device(0)
     device = torch.cuda.current_device()
@@ -441,7 +445,7 @@ def run_gpu_arm(args):
     ms = ev0.elapsed_time(ev1)
     kernels = plan.kernel_count() - kernels_before            # this rank's launches, timed region
     if dist is not None:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if dist.get_backend() == "gloo" else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_per_step = ms / args.steps
@@ -549,7 +553,7 @@ def run_gpu_arm(args):
             download()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
-        tt = torch.tensor([dt], device="cuda")
+        tt = torch.tensor([dt], device="cpu" if dist is not None and dist.get_backend() == "gloo" else "cuda")
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
@@ -660,7 +664,10 @@ def run_gpu_arm(args):
                        "k": k, "arith": args.arith, "grid_bytes_per_gpu": grid_bytes,
                        "l2": (f"inputs larger than L2 ({grid_bytes / 1e6:.0f} MB grid vs 126 MB L2)"
                               if grid_bytes > (126 << 20) else "grid fits in L2"),
-                       "parallelism": (f"slab{world}" if world > 1 else "single")},
+                       "parallelism": (f"slab{world}" if world > 1 else "single"),
+                       **({"test_mode": "SB200_SHARE_GPU: all ranks on one GPU over gloo, host-staged exchange -- "
+                                        "a code-path check, not a scaling measurement"}
+                          if world > 1 and os.environ.get("SB200_SHARE_GPU") else {})},
             "roofline": roofline, "stencil_roofline": stencil_roofline,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": kernels * world,

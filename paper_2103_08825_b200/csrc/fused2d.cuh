@@ -31,7 +31,10 @@
 
 namespace sb {
 
-constexpr int F2_VX = 4;                 // columns per lane
+#ifndef SB_F2_VX
+#define SB_F2_VX 4
+#endif
+constexpr int F2_VX = SB_F2_VX;          // columns per lane
 constexpr int F2_CW = 32 * F2_VX;        // computed strip width
 #ifndef SB_F2_WARPS
 #define SB_F2_WARPS 4

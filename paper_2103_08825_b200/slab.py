@@ -180,22 +180,53 @@ class SlabSweep:
         return self.backend.download(out)
 
     # -- halo exchange: my edge planes -> neighbours' ghost planes
+    def _post(self, specs):
+        """Post grouped point-to-point transfers; ``specs`` = [(is_send, tensor,
+        peer)].  Returns a callable that completes them (on the current stream).
+
+        NCCL (one GPU per rank) and the CPU tests move the tensors as they are.
+        A ``gloo`` group over CUDA tensors is the TEST transport of the
+        shared-GPU emulation (two ranks on one device, tests/test_slab.py,
+        ``SB200_SHARE_GPU``): gloo moves host memory only, so the planes are
+        staged through the host around the same isend/irecv calls."""
+        import torch.distributed as dist
+        staged = bool(specs) and specs[0][1].is_cuda and dist.get_backend(self.group) == "gloo"
+        if not staged:
+            ops = [dist.P2POp(dist.isend if snd else dist.irecv, t, peer, self.group) for snd, t, peer in specs]
+            reqs = dist.batch_isend_irecv(ops)
+            return lambda: [req.wait() for req in reqs]
+        import torch
+        host = [t.cpu() if snd else torch.empty(t.shape, dtype=t.dtype) for snd, t, _ in specs]
+        reqs = [(dist.isend if snd else dist.irecv)(h, peer, group=self.group)
+                for (snd, _, peer), h in zip(specs, host)]
+
+        def finish():
+            for req in reqs:
+                req.wait()
+            for (snd, t, _), h in zip(specs, host):
+                if not snd:
+                    t.copy_(h)
+        return finish
+
+    def _edge_specs(self, which: int):
+        """(is_send, planes, peer) of this rank's edge planes and ghost planes in
+        buffer `which` (0 = current, 1 = other)."""
+        g = self.geom
+        specs = []
+        if g.ghost_lo:
+            G = g.ghost_lo
+            specs.append((True, self.backend.planes(0, G, which), self.rank - 1))
+            specs.append((False, self.backend.planes(-G, G, which), self.rank - 1))
+        if g.ghost_hi:
+            G = g.ghost_hi
+            specs.append((True, self.backend.planes(g.n - G, G, which), self.rank + 1))
+            specs.append((False, self.backend.planes(g.n, G, which), self.rank + 1))
+        return specs
+
     def exchange(self):
         if self.world == 1:
             return
-        import torch.distributed as dist
-        g = self.geom
-        ops = []
-        if g.ghost_lo:
-            G = g.ghost_lo
-            ops.append(dist.P2POp(dist.isend, self.backend.planes(0, G), self.rank - 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.backend.planes(-G, G), self.rank - 1, self.group))
-        if g.ghost_hi:
-            G = g.ghost_hi
-            ops.append(dist.P2POp(dist.isend, self.backend.planes(g.n - G, G), self.rank + 1, self.group))
-            ops.append(dist.P2POp(dist.irecv, self.backend.planes(g.n, G), self.rank + 1, self.group))
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
+        self._post(self._edge_specs(0))()
         self.exchanges += 1
 
     def run(self, steps: int, overlap: bool | None = None):
@@ -224,7 +255,6 @@ class SlabSweep:
         interior [G, n-G) meanwhile on the main stream (completing the step);
         the next interval's launches wait for the received ghost planes.  The
         first interval exchanges the uploaded edges up front."""
-        import torch.distributed as dist
         g = self.geom
         cuda = isinstance(self.backend, DeviceSlab)
         if cuda:
@@ -245,29 +275,19 @@ class SlabSweep:
                 self.backend.launch_range(kk, 0, e_lo, False)
             if g.ghost_hi:
                 self.backend.launch_range(kk, e_hi, g.n, False)
-            ops = []
-            if g.ghost_lo:
-                G = g.ghost_lo
-                ops.append(dist.P2POp(dist.isend, self.backend.planes(0, G, 1), self.rank - 1, self.group))
-                ops.append(dist.P2POp(dist.irecv, self.backend.planes(-G, G, 1), self.rank - 1, self.group))
-            if g.ghost_hi:
-                G = g.ghost_hi
-                ops.append(dist.P2POp(dist.isend, self.backend.planes(g.n - G, G, 1), self.rank + 1, self.group))
-                ops.append(dist.P2POp(dist.irecv, self.backend.planes(g.n, G, 1), self.rank + 1, self.group))
+            specs = self._edge_specs(1)
             if cuda:
                 ev = torch.cuda.Event()
                 ev.record(main)
                 with torch.cuda.stream(comm):
                     comm.wait_event(ev)
-                    reqs = dist.batch_isend_irecv(ops)
+                    finish = self._post(specs)
                 self.backend.launch_range(kk, e_lo, e_hi, True)     # interior, concurrent with the exchange
                 with torch.cuda.stream(main):                       # main stream waits for the ghosts
-                    for req in reqs:
-                        req.wait()
+                    finish()
                     main.wait_stream(comm)
             else:
-                for req in dist.batch_isend_irecv(ops):
-                    req.wait()
+                self._post(specs)()
                 self.backend.launch_range(kk, e_lo, e_hi, True)
             self.exchanges += 1
             done += kk

@@ -117,6 +117,61 @@ def test_gloo_world2_bit_identical(cfg, dims, k, steps, overlap):
     assert nex >= steps // k
 
 
+def _device_worker(rank, world, port, cfg, dims, k, steps, arith, outdir):
+    """One rank of the shared-GPU emulation: the real DeviceSlab path (sm_100a
+    kernels, range launches, plane views, main/communication streams) driven
+    through torch.distributed, every rank on cuda:0 with the gloo test
+    transport (SlabSweep._post stages the planes through the host)."""
+    import torch.distributed as dist
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    spec = config_spec(cfg)
+    gbox = seeded_box(dims, spec.r, seed=11)
+    sw = SlabSweep(spec, dims, rank=rank, world=world, k=k, arith=arith, device=0, stream_ptr=stream.cuda_stream)
+    sw.upload(sw.local_box(gbox))
+    sw.run(steps)
+    torch.cuda.synchronize()
+    out = sw.download()
+    np.save(os.path.join(outdir, f"r{rank}.npy"), out[sw.geom.interior_slice()])
+    np.save(os.path.join(outdir, f"x{rank}.npy"), np.array([sw.exchanges]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,dims,k,steps,arith,world", [
+    ("c2", (200000,), 16, 50, "exact", 2),      # 1D: exchange before each launch
+    ("c5", (64, 70, 130), 2, 9, "exact", 2),    # 3D box3d: edges, exchange on the comm stream, interior
+    ("c4", (96, 70, 66), 2, 9, "fma", 3),       # composed 3D star, three ranks (a middle slab with two ghost sides)
+    ("c3b", (400, 300), 4, 13, "exact", 2),
+    ("c3a", (600, 500), 32, 70, "fma", 2),      # separable composed 2D on slabs
+])
+def test_torch_distributed_ranks_on_one_gpu_bit_identical(cfg, dims, k, steps, arith, world):
+    """SlabSweep.run / _run_overlapped through torch.distributed with real
+    device slabs: bit-identical to the undecomposed sweep on one plan."""
+    import torch.multiprocessing as mp
+    from paper_2103_08825_b200.plan import Plan
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_device_worker, args=(world, _free_port(), cfg, dims, k, steps, arith, td), nprocs=world, join=True)
+        got = np.concatenate([np.load(os.path.join(td, f"r{r}.npy")) for r in range(world)], axis=0)
+        nex = int(np.load(os.path.join(td, "x0.npy"))[0])
+    spec = config_spec(cfg)
+    gbox = seeded_box(dims, spec.r, seed=11)
+    with Plan(spec, dims, k=k, arith=arith, device=0) as p:
+        p.upload(gbox)
+        p.run(steps)
+        want = p.download()
+    r = spec.r
+    assert got.tobytes() == want[r:r + dims[0]].tobytes()
+    if arith == "exact":
+        offs, ws = canonical(spec)
+        ref = c_oracle.sweep(gbox, r, offs, ws, steps)
+        assert got.tobytes() == ref[r:r + dims[0]].tobytes()
+    assert nex >= steps // k
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("cfg,dims,k,g", [
     ("c2", (300000,), 16, 2), ("c2", (300000,), 8, 4), ("c1", (100003,), 8, 3),
