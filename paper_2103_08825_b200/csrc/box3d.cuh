@@ -56,6 +56,13 @@ namespace sb {
 #define SB_B3_NS0 3
 #endif
 constexpr int B3_NS0 = SB_B3_NS0;   // TMA ring depth (level-0 planes)
+// fp32 pair path: the dx = 0 term of a point pair as two scalar FFMAs on the
+// halves of the accumulator pair (1) or as one FFMA2 on an assembled /
+// shifted-copy input pair (0)
+#ifndef SB_B3_MIDSCALAR
+#define SB_B3_MIDSCALAR 1
+#endif
+constexpr bool B3_MIDSCALAR = SB_B3_MIDSCALAR != 0;
 
 template <typename T, int NW>
 struct B3Geo {
@@ -68,7 +75,7 @@ struct B3Geo {
     static constexpr unsigned BOX_BYTES = PW * PH * sizeof(T);
     static constexpr int NJOBS = 2 + (TY + 2 + 31) / 32;     // ring jobs: 2 rows + column pairs
     // level-0 slots + two level-1 planes (+ two shifted copies for the fp32 pair path)
-    static constexpr int SMEM = (B3_NS0 + (sizeof(T) == 4 ? 4 : 2)) * ELEMS * (int)sizeof(T);
+    static constexpr int SMEM = (B3_NS0 + (sizeof(T) == 4 && !B3_MIDSCALAR ? 4 : 2)) * ELEMS * (int)sizeof(T);
 };
 
 template <typename T>
@@ -173,6 +180,53 @@ __device__ __forceinline__ unsigned long long b3_ffma2(unsigned long long w2, un
     return d;
 }
 
+// acc.lo += w * u0, acc.hi += w * u1: the dx = 0 term of a point pair, whose
+// inputs (u0, u1) straddle the two aligned 8 B loads.  As ONE FFMA2 the input
+// pair has to be assembled in a fresh aligned register pair, and ptxas rebuilds
+// it for every use (two moves per FFMA2: ~100 MOV / IMAD.MOV per warp and plane
+// beside 243 FFMA2 in the C5 kernel); two scalar FFMAs on the halves of the
+// accumulator pair take the same two FMA-pipe cycles and no moves.
+__device__ __forceinline__ unsigned long long b3_fma_mid(unsigned long long acc, float w, float u0, float u1) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(acc));
+    lo = fmaf(w, u0, lo);
+    hi = fmaf(w, u1, hi);
+    unsigned long long d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+    return d;
+}
+
+template <int RPT, int PW>
+__device__ __forceinline__ void b3_push_pair_mid(const float* p, B3Acc<float, true, RPT>& C, B3Acc<float, true, RPT>& K,
+                                                 B3Acc<float, true, RPT>& S, const unsigned long long* wpp,
+                                                 const float* w) {
+#pragma unroll
+    for (int r = 0; r < RPT + 2; r++) {
+        const unsigned long long a = *reinterpret_cast<const unsigned long long*>(p + r * PW);       // (u-1, u0)
+        const unsigned long long b = *reinterpret_cast<const unsigned long long*>(p + r * PW + 2);   // (u1, u2)
+        float um, u0, u1, u2;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(um), "=f"(u0) : "l"(a));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(u1), "=f"(u2) : "l"(b));
+        (void)um;
+        (void)u2;
+#pragma unroll
+        for (int i = 0; i < RPT; i++) {
+            const int dy = r - i - 1;
+            if (dy < -1 || dy > 1) continue;
+            const int q = (dy + 1) * 3;
+            C.v[i] = b3_ffma2(wpp[18 + q], a, C.v[i]);
+            K.v[i] = b3_ffma2(wpp[9 + q], a, K.v[i]);
+            S.v[i] = b3_ffma2(wpp[q], a, q == 0 ? 0ull : S.v[i]);
+            C.v[i] = b3_fma_mid(C.v[i], w[18 + q + 1], u0, u1);
+            K.v[i] = b3_fma_mid(K.v[i], w[9 + q + 1], u0, u1);
+            S.v[i] = b3_fma_mid(S.v[i], w[q + 1], u0, u1);
+            C.v[i] = b3_ffma2(wpp[18 + q + 2], b, C.v[i]);
+            K.v[i] = b3_ffma2(wpp[9 + q + 2], b, K.v[i]);
+            S.v[i] = b3_ffma2(wpp[q + 2], b, S.v[i]);
+        }
+    }
+}
+
 template <int RPT, int PW, bool SHIFTED>
 __device__ __forceinline__ void b3_push_pair(const float* p, const float* pm, B3Acc<float, true, RPT>& C,
                                              B3Acc<float, true, RPT>& K, B3Acc<float, true, RPT>& S,
@@ -210,7 +264,10 @@ __device__ __forceinline__ void b3_push_pair(const float* p, const float* pm, B3
 template <typename T, bool PAIR, bool FMA, int RPT, int PW, bool SHIFTED = false>
 __device__ __forceinline__ void b3_fold(const T* p, const T* pm, B3Acc<T, PAIR, RPT>& C, B3Acc<T, PAIR, RPT>& K,
                                         B3Acc<T, PAIR, RPT>& S, const Box3DParams<T>& P) {
-    if constexpr (PAIR)
+    if constexpr (PAIR && B3_MIDSCALAR)
+        b3_push_pair_mid<RPT, PW>(reinterpret_cast<const float*>(p), C, K, S, P.wpp,
+                                  reinterpret_cast<const float*>(P.w));
+    else if constexpr (PAIR)
         b3_push_pair<RPT, PW, SHIFTED>(reinterpret_cast<const float*>(p), reinterpret_cast<const float*>(pm), C, K,
                                        S, P.wpp);
     else
@@ -233,7 +290,7 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
     constexpr bool PAIR = sizeof(T) == 4 && FMA;
     // fp32 pairs: level-1 planes also get a copy shifted right by one column,
     // so level 2 loads all three input pairs aligned
-    constexpr bool SHIFTED = PAIR;
+    constexpr bool SHIFTED = PAIR && !B3_MIDSCALAR;
     constexpr bool UNROLL3 = U3;
     extern __shared__ __align__(1024) unsigned char smem_b3[];
     T* s0 = reinterpret_cast<T*>(smem_b3);      // B3_NS0 level-0 slots
