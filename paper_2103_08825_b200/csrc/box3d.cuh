@@ -366,6 +366,14 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
         int slot = gslot;
         unsigned phase = gphase;
 
+        // level-2 stores: the lane's 2 x 4 outputs of plane zs0 (the pointer advances one
+        // plane per stored plane); mode 2 = all four rows as aligned vectors, 1 = partial
+        // (tiles on the domain edge), 0 = nothing to store
+        const int xs = x0 + 2 * lane;
+        const int nrow = min(4, P.ny - (y0 + 4 * warp));
+        const int st_mode = (xs + 1 < P.nx && nrow == 4) ? 2 : ((xs < P.nx && nrow > 0) ? 1 : 0);
+        T* orow = P.dst + P.origin + (int64_t)zs0 * P.sz + (int64_t)(y0 + 4 * warp) * P.sy + xs;
+
         B3Acc<T, PAIR, 4> A[3], B[3];     // level 1 / level 2 pending sums, main points (roles rotate)
         B3Acc<T, PAIR, 1> R[3];           // level 1, ring job
 #pragma unroll
@@ -440,22 +448,32 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
         auto level2 = [&](int t, auto rot, const T* l1) {
             constexpr int ROT = decltype(rot)::value;
             constexpr int IC = ROT, IK = (ROT + 1) % 3, IS = (ROT + 2) % 3;
-            b3_fold<T, PAIR, FMA, 4, PW, SHIFTED>(l1 + (4 * warp) * PW + 2 * lane, l1 + 2 * PLANE + (4 * warp) * PW +
-                                                  2 * lane + 2, B[IC], B[IK], B[IS], P);
-            const int zc = p_first + t - 2;
-            if (zc >= zs0 && zc < zs1) {
-                const int xs = x0 + 2 * lane;
-                const int nrow = min(4, P.ny - (y0 + 4 * warp));
-                T* row = P.dst + P.origin + (int64_t)zc * P.sz + (int64_t)(y0 + 4 * warp) * P.sy + xs;
-                if (xs + 1 < P.nx) {
+            // (the level-1 planes of arrivals 0 and 1 lie below every output's cone: no fold;
+            // the sets they would have started complete at t = 2, 3, before the first store)
+            if (t >= 2)
+                b3_fold<T, PAIR, FMA, 4, PW, SHIFTED>(l1 + (4 * warp) * PW + 2 * lane, l1 + 2 * PLANE + (4 * warp) * PW +
+                                                      2 * lane + 2, B[IC], B[IK], B[IS], P);
+            // output plane zc = zs0 + (t - 4): inside [zs0, zs1) exactly for 4 <= t < M
+            if (t >= 4) {
+                if (st_mode == 2) {
+                    T* r1 = orow + P.sy;
+                    T* r2 = r1 + P.sy;
+                    b3_st2(orow, B[IC], 0);
+                    b3_st2(r1, B[IC], 1);
+                    b3_st2(r2, B[IC], 2);
+                    b3_st2(r2 + P.sy, B[IC], 3);
+                } else if (st_mode == 1) {      // domain-edge tiles: short rows / odd last column
+                    if (xs + 1 < P.nx) {
 #pragma unroll
-                    for (int i = 0; i < 4; i++)
-                        if (i < nrow) b3_st2(row + i * P.sy, B[IC], i);
-                } else if (xs < P.nx) {
+                        for (int i = 0; i < 4; i++)
+                            if (i < nrow) b3_st2(orow + i * P.sy, B[IC], i);
+                    } else {
 #pragma unroll
-                    for (int i = 0; i < 4; i++)
-                        if (i < nrow) row[i * P.sy] = B[IC].get(i, 0);
+                        for (int i = 0; i < 4; i++)
+                            if (i < nrow) orow[i * P.sy] = B[IC].get(i, 0);
+                    }
                 }
+                orow += P.sz;
             }
         };
         auto next_slot = [&]() {

@@ -361,14 +361,21 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     // per-die work queues (402), a warp-specialised level split (335)
     static const int nw = (int)env_double("SB200_B3_NW", 4);
     static const int minb = (int)env_double("SB200_B3_MINB", 0);
-    // fp32: the 3x-unrolled loop (roles renamed, no accumulator moves on the FMA pipe)
-    // measured 630 vs 600-635 GStencil/s on C5 fp32
-    static const int u3 = (int)env_double("SB200_B3_U3", 1);
+    // fp32: with the scalar dx = 0 term (no input-pair moves) the single-copy loop wins
+    // (C5 fp32: 713 vs 691 GStencil/s for the 3x-unrolled, role-renamed one; 5 or 6
+    // CTAs/SM, SB200_B3_MINB, measured equal: 700-712)
+    static const int u3 = (int)env_double("SB200_B3_U3", 0);
     if constexpr (sizeof(T) == 4 && FMA) {
         if (u3 && nw == 8) return launch_box3d<T, FMA, 8, 2, true>(P, src_idx);
+        if (u3 && minb == 6) return launch_box3d<T, FMA, 4, 6, true>(P, src_idx);
+        if (u3 && minb == 5) return launch_box3d<T, FMA, 4, 5, true>(P, src_idx);
         if (u3) return launch_box3d<T, FMA, 4, 4, true>(P, src_idx);
     }
     if (nw == 8) return launch_box3d<T, FMA, 8, 2>(P, src_idx);
+    if constexpr (sizeof(T) == 4 && FMA) {
+        if (minb == 5) return launch_box3d<T, FMA, 4, 5>(P, src_idx);
+        if (minb == 6) return launch_box3d<T, FMA, 4, 6>(P, src_idx);
+    }
     if (minb == 3) return launch_box3d<T, FMA, 4, 3>(P, src_idx);
     return launch_box3d<T, FMA, 4, 4>(P, src_idx);
 }
