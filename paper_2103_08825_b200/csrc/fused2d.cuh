@@ -50,7 +50,7 @@ struct Item2D {
     int32_t tix;     // strip index
     int32_t ys0;     // output rows [ys0, ys1)
     int32_t ys1;
-    int32_t pad;
+    int32_t plain;   // 1: the whole dependency cone is interior (plain2d.cuh)
 };
 
 template <typename T>
@@ -141,31 +141,19 @@ __device__ __forceinline__ void f2_push3(const T (&u)[F2_VX + 2], T (&Pm)[F2_VX]
     }
 }
 
-template <typename T, bool BOX, int K, bool FMA, bool SEP = false>
-__global__ void __launch_bounds__(F2_WARPS * 32)
-fused2d_kernel(const Fused2DParams<T> P) {
+// One (strip, y-range) item of the general kernel, run by one warp on its ring of
+// F2_DEPTH + K shared rows: prefetch distance F2_DEPTH - 1 plus the K rows already
+// consumed (their x-halo columns are the Dirichlet values of the rows completed by
+// levels 1..K: no global reload on the edge strips).
+// shared row layout: [VEC-1] left edge, [VEC..VEC+CW) strip columns, [VEC+CW] right edge
+template <typename T, bool BOX, int K, bool FMA, bool SEP>
+__device__ __forceinline__ void fused2d_item(const Fused2DParams<T>& P, const Item2D it, T* ring, const int lane,
+                                             const unsigned item) {
     using TL = F2Tile<T, K>;
     constexpr int VEC = 16 / (int)sizeof(T);
     using V = typename Vec16<T>::type;
-    extern __shared__ __align__(16) unsigned char smem_f2[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // ring of RING rows per warp: prefetch distance F2_DEPTH - 1 plus the K
-    // rows already consumed (their x-halo columns are the Dirichlet values of
-    // the rows completed by levels 1..K: no global reload on the edge strips)
     constexpr int RING = F2_DEPTH + K;
-    T* ring = reinterpret_cast<T*>(smem_f2) + warp * RING * F2_ROWW;
-    // shared row layout: [VEC-1] left edge, [VEC..VEC+CW) strip columns, [VEC+CW] right edge
-
-    auto claim_issue = [&]() -> unsigned {
-        unsigned id = 0;
-        if (lane == 0)
-            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(id) : "l"(&P.counter[0]) : "memory");
-        return id;
-    };
-    unsigned item = __shfl_sync(0xffffffffu, claim_issue(), 0);
-    while (item < (unsigned)P.items) {
-        const unsigned next_raw = claim_issue();        // resolved after this item
-        const Item2D it = P.sched[item];
+    {
         unsigned long long tr0 = 0;
         if (P.trace && lane == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
         const int x0 = TL::X0 + it.tix * TL::TXO;       // output strip origin
@@ -332,11 +320,28 @@ fused2d_kernel(const Fused2DParams<T> P) {
             unsigned smid;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-            P.trace[4 * item + 0] = ((unsigned long long)smid << 32) | (blockIdx.x * F2_WARPS + warp);
+            P.trace[4 * item + 0] = ((unsigned long long)smid << 32) | (blockIdx.x * F2_WARPS + (threadIdx.x >> 5));
             P.trace[4 * item + 1] = tr0;
             P.trace[4 * item + 2] = tr1;
             P.trace[4 * item + 3] = ((unsigned long long)it.tix << 40) | (unsigned long long)(it.ys1 - it.ys0);
         }
+    }
+}
+
+// Persistent warps over the item list: one atomic per claim, issued one item
+// ahead; the last warp to retire resets the queue for the next launch.
+template <typename T, typename ItemFn>
+__device__ __forceinline__ void f2_item_loop(const Fused2DParams<T>& P, const int lane, ItemFn&& run) {
+    auto claim_issue = [&]() -> unsigned {
+        unsigned id = 0;
+        if (lane == 0)
+            asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(id) : "l"(&P.counter[0]) : "memory");
+        return id;
+    };
+    unsigned item = __shfl_sync(0xffffffffu, claim_issue(), 0);
+    while (item < (unsigned)P.items) {
+        const unsigned next_raw = claim_issue();        // resolved after this item
+        run(P.sched[item], item);
         item = __shfl_sync(0xffffffffu, next_raw, 0);
     }
     if (lane == 0) {
@@ -346,6 +351,17 @@ fused2d_kernel(const Fused2DParams<T> P) {
             atomicExch(&P.counter[1], 0u);
         }
     }
+}
+
+template <typename T, bool BOX, int K, bool FMA, bool SEP = false>
+__global__ void __launch_bounds__(F2_WARPS * 32)
+fused2d_kernel(const Fused2DParams<T> P) {
+    extern __shared__ __align__(16) unsigned char smem_f2[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    T* ring = reinterpret_cast<T*>(smem_f2) + warp * (F2_DEPTH + K) * F2_ROWW;
+    f2_item_loop(P, lane, [&](const Item2D it, const unsigned item) {
+        fused2d_item<T, BOX, K, FMA, SEP>(P, it, ring, lane, item);
+    });
 }
 
 template <typename T, int K>

@@ -5,10 +5,19 @@
 
 #include <climits>
 #include <cmath>
+#include <type_traits>
 
 #include "plan.hpp"
 #include "fused2d.cuh"
+#include "plain2d.cuh"
 #include "sep2d.cuh"
+
+#ifndef SB_P2_MINB
+#define SB_P2_MINB 3      // CTAs per SM of split2d_kernel at K = 3, 4 (4: 128 registers, measured slower)
+#endif
+#ifndef SB_P2_MINB_K2
+#define SB_P2_MINB_K2 3   // ... at K = 2 (HBM-bound)
+#endif
 
 namespace sbh {
 namespace {
@@ -44,7 +53,7 @@ std::vector<sb::Item2D> guided_schedule_2d(int tiles_x, int64_t ny, int64_t warp
                 it.tix = t;
                 it.ys0 = (int32_t)pos[t];
                 it.ys1 = (int32_t)(pos[t] + l);
-                it.pad = 0;
+                it.plain = 0;
                 out.push_back(it);
                 pos[t] += l;
                 done += l;
@@ -80,10 +89,72 @@ bool separable_weights(const sb_plan* P, double a[3], double b[3]) {
     return true;
 }
 
+// Split a guided schedule into the items whose whole K-level dependency cone is
+// interior (plain2d_kernel) and the rest (fused2d_kernel): strips that touch an x
+// halo column, and the K - 1 rows next to a physical y side of every other strip.
+template <int K>
+void split_plain_2d(const sb_plan* P, const std::vector<sb::Item2D>& items, std::vector<sb::Item2D>& plain,
+                    std::vector<sb::Item2D>& edge) {
+    using TL = sb::F2Tile<double, K>;
+    const int64_t nx = P->dims[1], ny = P->dims[0];
+    const int64_t row_lo = -P->hlo, row_hi = ny + P->hhi;
+    // output rows whose level-1..K cone stays inside computed rows and whose level-0 rows are allocated
+    const int64_t plo = std::max<int64_t>(P->phys_lo ? K - 1 : INT_MIN / 2, row_lo + K);
+    // (plain2d_kernel prefetches P2_DIST rows past an item without testing: they must be allocated)
+    const int64_t phi = std::min<int64_t>(P->phys_hi ? ny - (K - 1) : INT_MAX / 2, row_hi - 2 * K - sb::P2_DIST);   // (+ K - 1 more level-0 rows in the skewed form)
+    static const int min_rows = (int)env_double("SB200_2D_PLAIN_MIN_ROWS", 8);
+    for (const auto& it : items) {
+        const int64_t xc = (int64_t)TL::X0 + (int64_t)it.tix * TL::TXO - TL::HL;
+        const bool xplain = xc >= 0 && xc + sb::F2_CW <= nx;   // every computed column interior, edge columns in [-1, nx]
+        const int64_t lo = std::max<int64_t>(it.ys0, plo), hi = std::min<int64_t>(it.ys1, phi);
+        if (!xplain || hi - lo < min_rows) {
+            edge.push_back(it);
+            continue;
+        }
+        sb::Item2D e = it;
+        if (lo > it.ys0) {
+            e.ys0 = it.ys0;
+            e.ys1 = (int32_t)lo;
+            edge.push_back(e);
+        }
+        if (hi < it.ys1) {
+            e.ys0 = (int32_t)hi;
+            e.ys1 = it.ys1;
+            edge.push_back(e);
+        }
+        e.ys0 = (int32_t)lo;
+        e.ys1 = (int32_t)hi;
+        plain.push_back(e);
+    }
+}
+
+int upload_items(sb_plan* P, const std::vector<sb::Item2D>& items, void** d) {
+    *d = nullptr;
+    if (items.empty()) return SB_OK;
+    SB_CUDA(cudaMalloc(d, sizeof(sb::Item2D) * items.size()));
+    // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and the
+    // kernel runs on the (non-blocking) plan stream
+    SB_CUDA(cudaMemcpyAsync(*d, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice, P->stream));
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
+}
+
 template <typename T, bool BOX, int K, bool FMA, bool SEP>
 int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     using TL = sb::F2Tile<T, K>;
-    auto kern = sb::fused2d_kernel<T, BOX, K, FMA, SEP>;
+    // fp64, K = 2..4: the halo-free items run the lean path of split2d_kernel (plain2d.cuh);
+    // SB200_2D_PLAIN=0: every item on fused2d_kernel
+    constexpr bool HAS_PLAIN = std::is_same<T, double>::value && K >= 2 && K <= 4;
+    static const int plain_on = (int)env_double("SB200_2D_PLAIN", 1);
+    static const int plain_skew = (int)env_double("SB200_2D_SKEW", 1);
+    static const int edge_rows = (int)env_double("SB200_2D_EDGE_ROWS", 128);   // cap on the rows of a halo item (0: none): long ones are the tail of the launch (C3b k=4 1058 -> 1216)
+    const bool split = HAS_PLAIN && plain_on;
+    void (*kern)(const sb::Fused2DParams<T>) = sb::fused2d_kernel<T, BOX, K, FMA, SEP>;
+    if constexpr (HAS_PLAIN) {
+        if (split)
+            kern = plain_skew ? sb::split2d_kernel<BOX, K, FMA, SEP, (K == 2 ? SB_P2_MINB_K2 : SB_P2_MINB), true>
+                              : sb::split2d_kernel<BOX, K, FMA, SEP, (K == 2 ? SB_P2_MINB_K2 : SB_P2_MINB), false>;
+    }
     const int smem = sb::fused2d_smem_bytes<T, K>();
     Sched1D* sc = nullptr;
     const int64_t y_lo = range_lo(P), y_hi = range_hi(P);
@@ -102,15 +173,32 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
             it.ys0 += (int32_t)y_lo;
             it.ys1 += (int32_t)y_lo;
         }
+        if (split) {
+            // halo items first (they start with the launch: the general path is slower per row),
+            // then the plain ones, each group in guided order
+            std::vector<sb::Item2D> plain, edge;
+            split_plain_2d<K>(P, items, plain, edge);
+            items.clear();
+            for (const auto& it : edge) {
+                const int32_t step = edge_rows > 0 ? edge_rows : it.ys1 - it.ys0;
+                for (int32_t y = it.ys0; y < it.ys1; y += step) {
+                    sb::Item2D c = it;
+                    c.ys0 = y;
+                    c.ys1 = std::min<int32_t>(y + step, it.ys1);
+                    c.plain = 0;
+                    items.push_back(c);
+                }
+            }
+            for (auto it : plain) {
+                it.plain = 1;
+                items.push_back(it);
+            }
+        }
         e.comp_lo = y_lo;
         e.comp_hi = y_hi;
         e.nchunks = (int)items.size();
-        SB_CUDA(cudaMalloc(&e.d_chunks, sizeof(sb::Item2D) * items.size()));
-        // stream-ordered: a pageable cudaMemcpy may return before its DMA lands, and the
-        // kernel runs on the (non-blocking) plan stream
-        SB_CUDA(cudaMemcpyAsync(e.d_chunks, items.data(), sizeof(sb::Item2D) * items.size(), cudaMemcpyHostToDevice,
-                                P->stream));
-        SB_CUDA(cudaStreamSynchronize(P->stream));
+        const int rc = upload_items(P, items, &e.d_chunks);
+        if (rc != SB_OK) return rc;
         P->sched1d.push_back(e);
         sc = &P->sched1d.back();
     }
@@ -149,9 +237,11 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
             prm.sb[i] = (T)b[i];
         }
     }
-    P->last_kernel = "fused2d_kernel";
-    kern<<<(unsigned)blocks, sb::F2_WARPS * 32, smem, P->stream>>>(prm);
-    SB_CUDA(cudaGetLastError());
+    P->last_kernel = split ? "split2d_kernel" : "fused2d_kernel";
+    if (blocks > 0) {
+        kern<<<(unsigned)blocks, sb::F2_WARPS * 32, smem, P->stream>>>(prm);
+        SB_CUDA(cudaGetLastError());
+    }
     return SB_OK;
 }
 

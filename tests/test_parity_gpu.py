@@ -364,7 +364,7 @@ def test_sep2d_composed_within_fp64_bar(k, dims, halo):
             p.upload(box)
             t = p.run(T)
             got = p.download()
-        assert t.kernel_name.startswith("sep2d") or t.kernel_name == "fused2d_kernel"
+        assert t.kernel_name.startswith("sep2d") or t.kernel_name in ("fused2d_kernel", "split2d_kernel")
         want = oracle(spec, box, T)
         assert np_oracle.max_rel_error(interior(got, 1), interior(want, 1)) <= FP64_TOL
         mask = np.ones(box.shape, bool)
@@ -505,6 +505,38 @@ def test_fused2d_fp32():
     want = c_oracle.sweep(box32.astype(np.float64), 1, offs, [float(np.float32(w)) for w in ws], 24)
     got = sweep(spec, box32, 24, arith="fma", kernel="fused", k=8)
     assert np_oracle.max_rel_error(got, want) <= FP32_TOL
+
+
+# split2d_kernel: the halo-free (strip, y-range) items of a k = 2 / 4 fp64 launch run the lean
+# path (plain2d.cuh), the rest the general one, in one launch (launch2d.cu split_plain_2d);
+# grids wide and tall enough to have plain strips, ragged last strips, and T not a multiple
+# of k (tails on the k = 1 path)
+@pytest.mark.parametrize("cfg", ["c3a", "c3b"])
+@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("dims", [(64, 400), (700, 1500), (1025, 2049), (23, 260)])
+def test_plain2d_split_exact(cfg, k, dims):
+    spec = config_spec(cfg)
+    box = seeded_box(dims, 1, seed=sum(dims) + k)
+    T = 10
+    got = sweep(spec, box, T, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, T).tobytes()
+
+
+@pytest.mark.parametrize("k", [2, 4])
+@pytest.mark.parametrize("halo", ["zero", "full"])
+def test_plain2d_split_star_and_fma(k, halo):
+    box = seeded_box((900, 1300), 1, seed=k, halo=halo)
+    spec = make_stencil_spec("2d5p")
+    got = sweep(spec, box, 12, arith="exact", kernel="fused", k=k)
+    assert got.tobytes() == oracle(spec, box, 12).tobytes()
+    for cfg in ("c3a", "c3b"):     # c3a: the separable push (rank-1 weights), c3b: 9 terms
+        spec = config_spec(cfg)
+        got = sweep(spec, box, 12, arith="fma", kernel="fused", k=k)
+        assert np_oracle.max_rel_error(got, oracle(spec, box, 12)) <= FP64_TOL
+        r = 1
+        mask = np.ones(got.shape, bool)
+        mask[r:-r, r:-r] = False
+        assert np.array_equal(got[mask], box[mask])          # halo untouched
 
 
 @pytest.mark.parametrize("cfg", ["c3a", "c3b"])

@@ -31,5 +31,5 @@ cap c2_compose1d c2 compose1d 10 ""
 cap c1_compose1d c1 compose1d 1 ""
 cap c3a_sep_vpass c3a sep_vpass 5 ""
 cap c3a_sep_hpass c3a sep_hpass 5 ""
-cap c3b_fused2d c3b fused2d 20 ""
+cap c3b_split2d c3b split2d 20 ""
 echo done > $O/DONE
