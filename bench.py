@@ -312,7 +312,7 @@ def kernel_label(spec, wl, k, arith):
     if d == 2:
         if k >= 16:
             return f"sep_vpass_kernel + sep_hpass_kernel (K={k}, separable composed)"
-        if wl.get("dtype", "f64") == "f64" and k in (2, 4):
+        if wl.get("dtype", "f64") == "f64" and k == 4:
             return f"split2d_kernel (K={k}: halo-free items on the lean path, plain2d.cuh)"
         return f"fused2d_kernel (K={k})"
     if spec.shape == "star" and arith == "fma" and k == 2 and wl.get("dtype", "f64") == "f64":

@@ -15,9 +15,6 @@
 #ifndef SB_P2_MINB
 #define SB_P2_MINB 3      // CTAs per SM of split2d_kernel at K = 3, 4 (4: 128 registers, measured slower)
 #endif
-#ifndef SB_P2_MINB_K2
-#define SB_P2_MINB_K2 3   // ... at K = 2 (HBM-bound)
-#endif
 
 namespace sbh {
 namespace {
@@ -142,9 +139,10 @@ int upload_items(sb_plan* P, const std::vector<sb::Item2D>& items, void** d) {
 template <typename T, bool BOX, int K, bool FMA, bool SEP>
 int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     using TL = sb::F2Tile<T, K>;
-    // fp64, K = 2..4: the halo-free items run the lean path of split2d_kernel (plain2d.cuh);
-    // SB200_2D_PLAIN=0: every item on fused2d_kernel
-    constexpr bool HAS_PLAIN = std::is_same<T, double>::value && K >= 2 && K <= 4;
+    // fp64, K = 4: the halo-free items run the lean path of split2d_kernel (plain2d.cuh);
+    // SB200_2D_PLAIN=0: every item on fused2d_kernel.  (K = 2 is HBM-bound and measured
+    // slower on the split kernel at 3, 4 and 5 CTAs per SM: C3b 583-597 vs 619 GStencil/s.)
+    constexpr bool HAS_PLAIN = std::is_same<T, double>::value && K >= 3 && K <= 4;
     static const int plain_on = (int)env_double("SB200_2D_PLAIN", 1);
     static const int plain_skew = (int)env_double("SB200_2D_SKEW", 1);
     static const int edge_rows = (int)env_double("SB200_2D_EDGE_ROWS", 128);   // cap on the rows of a halo item (0: none): long ones are the tail of the launch (C3b k=4 1058 -> 1216)
@@ -152,8 +150,8 @@ int launch_fused2d_k(sb_plan* P, const T* src, T* dst) {
     void (*kern)(const sb::Fused2DParams<T>) = sb::fused2d_kernel<T, BOX, K, FMA, SEP>;
     if constexpr (HAS_PLAIN) {
         if (split)
-            kern = plain_skew ? sb::split2d_kernel<BOX, K, FMA, SEP, (K == 2 ? SB_P2_MINB_K2 : SB_P2_MINB), true>
-                              : sb::split2d_kernel<BOX, K, FMA, SEP, (K == 2 ? SB_P2_MINB_K2 : SB_P2_MINB), false>;
+            kern = plain_skew ? sb::split2d_kernel<BOX, K, FMA, SEP, SB_P2_MINB, true>
+                              : sb::split2d_kernel<BOX, K, FMA, SEP, SB_P2_MINB, false>;
     }
     const int smem = sb::fused2d_smem_bytes<T, K>();
     Sched1D* sc = nullptr;

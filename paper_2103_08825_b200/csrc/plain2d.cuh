@@ -37,8 +37,29 @@ namespace sb {
 
 constexpr int P2_RING = 9;     // staged rows per warp
 constexpr int P2_DIST = 8;     // prefetch distance (rows)
-constexpr int P2_ROWW = 136;   // doubles per shared row: [0,2) left edge pair, [2,130) strip, [130,132) right pair, pad
+// Shared row, in 16 B chunks: strip chunk q (columns 2q, 2q + 1 of the computed strip) at
+// position q + q / 8 -- one pad chunk per 8, so the 8 lanes of a 128-bit load phase (lane
+// L on chunks 2L, 2L + 1) fall on 8 different bank groups, where the dense layout gave
+// 2-way conflicts on every phase -- then the left / right strip-edge pairs at 72, 73 and
+// the dump chunk of the lanes that stage no edge at 74.
+constexpr int P2_ROWW = 150;   // doubles per shared row (75 chunks)
 constexpr int P2_ROWB = P2_ROWW * 8;
+__host__ __device__ constexpr int p2_pos(int q) { return q + (q >> 3); }
+
+__device__ __forceinline__ double2 p2_lds128(unsigned a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double p2_lds64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+// keep a per-lane constant in its register (ptxas otherwise rematerialises the lane
+// arithmetic inside the row loop: +7 instructions per row step)
+__device__ __forceinline__ void p2_pin(unsigned& x) { asm volatile("" : "+r"(x)); }
+__device__ __forceinline__ void p2_pin(int64_t& x) { asm volatile("" : "+l"(x)); }
 
 // SKEW: level l of row step t consumes the level-(l-1) row completed in step t - 1
 // (levels run top down inside a step, so the completed row is read before level
@@ -54,12 +75,23 @@ __device__ __forceinline__ void plain2d_item(const Fused2DParams<double>& P, con
     using TL = F2Tile<T, K>;
     static_assert(F2_VX == 4, "plain2d: 4 columns per lane");
     const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
-    const unsigned wr_s = ring_s + 16u + 16u * lane;                 // staging chunk of this lane (c = 0)
+    // staging: lane L copies chunks L and 32 + L (p2_pos(32 + L) = p2_pos(L) + 36)
+    unsigned wr_s = ring_s + 16u * (unsigned)p2_pos(lane);
     // strip-edge pairs: lane 0 columns [-2, 0), lane 1 columns [128, 130); the other lanes
-    // issue the same instruction with source size 0 (zero fill) into the row's pad
-    const unsigned we_s = ring_s + (lane == 0 ? 0u : lane == 1 ? 130u * 8u : 134u * 8u);
+    // issue the same instruction with source size 0 (zero fill) into the dump chunk
+    unsigned we_s = ring_s + 16u * (lane == 0 ? 72u : lane == 1 ? 73u : 74u);
     const unsigned esize = lane < 2 ? 16u : 0u;
-    const T* const rd = ring + 2 + F2_VX * lane;                      // own columns of slot 0
+    unsigned rd = ring_s + 16u * (unsigned)p2_pos(2 * lane);          // own columns of slot 0 (chunks 2L, 2L + 1)
+    // x-neighbours at level 1: column -1 (upper half of chunk 2L - 1, or of the left edge
+    // pair) and column 4 (lower half of chunk 2L + 2, or of the right edge pair)
+    const int nl = lane == 0 ? 2 * 72 + 1 : 2 * p2_pos(2 * lane - 1) + 1;
+    const int nr = lane == 31 ? 2 * 73 : 2 * p2_pos(2 * lane + 2);
+    unsigned rdl = ring_s + 8u * (unsigned)nl, rdr = ring_s + 8u * (unsigned)nr;
+    p2_pin(wr_s);
+    p2_pin(we_s);
+    p2_pin(rd);
+    p2_pin(rdl);
+    p2_pin(rdr);
     const bool stores = lane >= TL::HL / F2_VX && lane < 32 - TL::HL / F2_VX;
     const int eoff = lane == 0 ? -2 : lane == 1 ? F2_CW - 2 : 0;      // edge pair relative to the lane's chunk
     {
@@ -72,15 +104,31 @@ __device__ __forceinline__ void plain2d_item(const Fused2DParams<double>& P, con
 
         // one row into the ring slot at byte offset slot_b; unconditional: the host keeps
         // P2_DIST allocated rows below every plain item (split_plain_2d)
-        auto stage = [&](unsigned slot_b) {
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr_s + slot_b), "l"(gs));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr_s + slot_b + 512u), "l"(gs + 64));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(we_s + slot_b), "l"(gs + eoff), "r"(esize));
+        auto stage_from = [&](const T* g, unsigned slot_b) {
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr_s + slot_b), "l"(g));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wr_s + slot_b + 576u), "l"(g + 64));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(we_s + slot_b), "l"(g + eoff), "r"(esize));
             cp_async_commit();
-            gs += P.sy;
         };
 #pragma unroll
-        for (int t = 0; t < P2_DIST; t++) stage(t * P2_ROWB);
+        for (int t = 0; t < P2_DIST; t++) stage_from(gs + (int64_t)t * P.sy, t * P2_ROWB);
+        // The row loop is unrolled x3 and each of its three steps has its own staging and
+        // store pointer, advanced by three rows just before its use: a pointer bumped right
+        // after the cp.async / store that read it waits on that instruction's operand
+        // scoreboard (10% of the stall samples with one running pointer).
+        int64_t sy3b = 3 * (int64_t)sizeof(T) * P.sy;    // three rows, in bytes
+        p2_pin(sy3b);
+        auto bump = [&](auto*& ptr) {
+            using Ptr = std::remove_reference_t<decltype(ptr)>;
+            ptr = reinterpret_cast<Ptr>(reinterpret_cast<uintptr_t>(ptr) + (uintptr_t)sy3b);
+        };
+        const T* gsr[3];
+        T* outr[3];
+#pragma unroll
+        for (int q = 0; q < 3; q++) {
+            gsr[q] = gs + (int64_t)(P2_DIST + q - 3) * P.sy;
+            outr[q] = outp + (int64_t)(q - 3) * P.sy;
+        }
 
         T A[K][3][F2_VX];   // per level: pending-row sets, roles rotating with t (mod 3)
 #pragma unroll
@@ -98,17 +146,18 @@ __device__ __forceinline__ void plain2d_item(const Fused2DParams<double>& P, con
             constexpr int IC = ROT, IK = (ROT + 1) % 3, IS = (ROT + 2) % 3;
             cp_async_wait<P2_DIST - 1>();
             __syncwarp();
-            const T* row = reinterpret_cast<const T*>(reinterpret_cast<const unsigned char*>(rd) + b0) + ROT * P2_ROWW;
             T u[F2_VX + 2];
             {
-                const double2 a = *reinterpret_cast<const double2*>(row);
-                const double2 b = *reinterpret_cast<const double2*>(row + 2);
+                const unsigned sb = b0 + ROT * P2_ROWB;     // slot of row t
+                const double2 a = p2_lds128(rd + sb);
+                const double2 b = p2_lds128(rd + sb + 16u);
                 u[1] = a.x; u[2] = a.y; u[3] = b.x; u[4] = b.y;
-                u[0] = row[-1];
-                u[5] = row[F2_VX];
+                u[0] = p2_lds64(rdl + sb);
+                u[5] = p2_lds64(rdr + sb);
             }
             // restage the slot of row t - 1: every lane read it before the __syncwarp above
-            stage(ROT == 0 ? b2 + 2 * P2_ROWB : b0 + (ROT - 1) * P2_ROWB);
+            bump(gsr[ROT]);
+            stage_from(gsr[ROT], ROT == 0 ? b2 + 2 * P2_ROWB : b0 + (ROT - 1) * P2_ROWB);
             if constexpr (SKEW) {
                 T out[F2_VX];
 #pragma unroll
@@ -143,11 +192,11 @@ __device__ __forceinline__ void plain2d_item(const Fused2DParams<double>& P, con
                     for (int j = 0; j < F2_VX; j++) u[j + 1] = A[l - 1][IC][j];   // completed row p_first + t - l of level l
                 }
             }
+            bump(outr[ROT]);
             if (t >= LAG && stores) {                       // level-K row ys0 + t - LAG
-                *reinterpret_cast<double2*>(outp) = make_double2(u[1], u[2]);
-                *reinterpret_cast<double2*>(outp + 2) = make_double2(u[3], u[4]);
+                *reinterpret_cast<double2*>(outr[ROT]) = make_double2(u[1], u[2]);
+                *reinterpret_cast<double2*>(outr[ROT] + 2) = make_double2(u[3], u[4]);
             }
-            outp += P.sy;
         };
         for (int t = 0; t < M; t += 3) {
             row_step(t, std::integral_constant<int, 0>());
@@ -168,7 +217,7 @@ split2d_kernel(const Fused2DParams<double> P) {
     extern __shared__ __align__(16) unsigned char smem_f2[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double* ring = reinterpret_cast<double*>(smem_f2) + warp * (F2_DEPTH + K) * F2_ROWW;
-    static_assert(P2_RING * P2_ROWW <= (F2_DEPTH + 2) * F2_ROWW, "plain ring fits the general one");
+    static_assert(P2_RING * P2_ROWW <= (F2_DEPTH + 3) * F2_ROWW, "plain ring fits the general one");
     f2_item_loop(P, lane, [&](const Item2D it, const unsigned item) {
         if (it.plain)
             plain2d_item<BOX, K, FMA, SEP, SKEW>(P, it, ring, lane);

@@ -507,7 +507,7 @@ def test_fused2d_fp32():
     assert np_oracle.max_rel_error(got, want) <= FP32_TOL
 
 
-# split2d_kernel: the halo-free (strip, y-range) items of a k = 2 / 4 fp64 launch run the lean
+# split2d_kernel: the halo-free (strip, y-range) items of a k = 4 fp64 launch run the lean
 # path (plain2d.cuh), the rest the general one, in one launch (launch2d.cu split_plain_2d);
 # grids wide and tall enough to have plain strips, ragged last strips, and T not a multiple
 # of k (tails on the k = 1 path)
