@@ -78,6 +78,8 @@ struct B3Geo {
     static constexpr int SMEM = (B3_NS0 + (sizeof(T) == 4 && !B3_MIDSCALAR ? 4 : 2)) * ELEMS * (int)sizeof(T);
 };
 
+constexpr int B3_MAX_SEG = 47;
+
 template <typename T>
 struct Box3DParams {
     const T* src;
@@ -86,8 +88,10 @@ struct Box3DParams {
     int nx, ny, nz;
     int ax, ry, hz, hz_hi;   // allocation coordinates of interior (0,0,0); planes above
     int phys_lo, phys_hi;
-    int tiles_x, tiles_y, nseg, lz, items, total_ctas;
-    int z0, z1;              // output planes [z0, z1) of this launch (range launches)
+    int tiles_x, tiles_y, nseg, items, total_ctas;
+    // z segments of this launch's output planes: segment s = [zb[s], zb[s+1]), the same for
+    // every xy tile; lengths decrease (guided schedule: the last items are short)
+    int zb[B3_MAX_SEG + 1];
     unsigned int* counter;   // [0] next item, [1] retired CTAs
     T w[27];                 // w[(dz+1)*9 + (dy+1)*3 + (dx+1)]
     unsigned long long wpp[27];   // fp32: (w, w) pairs for the packed FFMA2 push
@@ -352,7 +356,7 @@ box3d_kernel(const __grid_constant__ CUtensorMap tmap, const Box3DParams<T> P) {
             m_out &= 0xffu;
             m_shell &= 0xffu;
         }
-        const int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);
+        const int zs0 = P.zb[seg], zs1 = P.zb[seg + 1];
         const int p_first = zs0 - 2;
         const int M = (zs1 - zs0) + 4;                          // level-0 arrivals
 

@@ -1,4 +1,5 @@
 // Launch unit of the fused 3D kernel (K3/K4): TMA descriptors, tile/segment work items.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -326,13 +327,44 @@ int launch_box3d(sb_plan* P, int src_idx) {
     prm.tiles_y = (int)((P->dims[1] + G::TY - 1) / G::TY);
     const int ctas_max = P->num_sms * occ;
     const int tiles = prm.tiles_x * prm.tiles_y;
+    // z segments, the same for every xy tile (items are claimed tile-fastest, so the CTAs
+    // running together work on neighbouring tiles of one z range and share halo lines in
+    // L2).  Equal segments (ITEMS_PER_CTA per CTA) until 1/GUIDE of the remaining planes per
+    // CTA is shorter, then guided lengths down to MIN planes -- the last items are short, so
+    // the CTAs finish together (equal segments only, SB200_B3_GUIDE=0: 7.8 rounds of items,
+    // 6-8% of the SM cycles idle at the end).
     const double per = env_double("SB200_B3_ITEMS_PER_CTA", 8.0);
+    const double guide = env_double("SB200_B3_GUIDE", 2.5);
+    const int64_t lmin = std::max<int64_t>(1, (int64_t)env_double("SB200_B3_MIN_PLANES", 12));
     const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
-    const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((nzr + nseg - 1) / nseg);
-    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
-    prm.z0 = (int)z_lo;
-    prm.z1 = (int)(z_lo + nzr);
+    int nb = 0;
+    prm.zb[0] = (int)z_lo;
+    if (guide > 0) {
+        // no segment longer than the equal split's: long first items let the CTAs drift apart
+        // in z and lose the L2 sharing (uncapped: C5 fp64 406 -> 393, fp32 704 -> 615 GStencil/s)
+        const int64_t neq = std::max<int64_t>(1, (int64_t)(per * ctas_max / tiles + 0.5));
+        const int64_t lmax = std::max<int64_t>(lmin, (nzr + neq - 1) / neq);
+        int64_t rem = nzr;
+        while (rem > 0) {
+            int64_t len = (int64_t)std::ceil((double)rem * tiles / (guide * ctas_max));
+            len = std::min(std::max(len, lmin), lmax);
+            if (nb == sb::B3_MAX_SEG - 1 || rem - len < lmin / 2) len = rem;
+            len = std::min(len, rem);
+            prm.zb[nb + 1] = prm.zb[nb] + (int)len;
+            nb++;
+            rem -= len;
+        }
+    } else {
+        const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nzr, sb::B3_MAX_SEG),
+                                                                   (int64_t)(per * ctas_max / tiles + 0.5)));
+        const int64_t lz = (nzr + nseg - 1) / nseg;
+        for (int64_t z = 0; z < nzr; z += lz) {
+            prm.zb[nb + 1] = (int)(z_lo + std::min(z + lz, nzr));
+            nb++;
+        }
+    }
+    for (int i = nb + 1; i <= sb::B3_MAX_SEG; i++) prm.zb[i] = prm.zb[nb];
+    prm.nseg = nb;
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
@@ -348,8 +380,10 @@ int launch_box3d(sb_plan* P, int src_idx) {
         prm.wpp[i] = ((unsigned long long)u << 32) | u;
     }
     P->last_kernel = "box3d_kernel";
-    kern<<<(unsigned)prm.total_ctas, G::THREADS, G::SMEM, P->stream>>>(P->tmap[GEO][src_idx], prm);
-    SB_CUDA(cudaGetLastError());
+    if (prm.items > 0) {
+        kern<<<(unsigned)prm.total_ctas, G::THREADS, G::SMEM, P->stream>>>(P->tmap[GEO][src_idx], prm);
+        SB_CUDA(cudaGetLastError());
+    }
     return SB_OK;
 }
 

@@ -194,8 +194,9 @@ __device__ __forceinline__ void plain2d_item(const Fused2DParams<double>& P, con
             }
             bump(outr[ROT]);
             if (t >= LAG && stores) {                       // level-K row ys0 + t - LAG
-                *reinterpret_cast<double2*>(outr[ROT]) = make_double2(u[1], u[2]);
-                *reinterpret_cast<double2*>(outr[ROT] + 2) = make_double2(u[3], u[4]);
+                // (global-space stores: the integer pointer bump hides the address space from nvcc)
+                asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(outr[ROT]), "d"(u[1]), "d"(u[2]) : "memory");
+                asm volatile("st.global.v2.f64 [%0+16], {%1, %2};" ::"l"(outr[ROT]), "d"(u[3]), "d"(u[4]) : "memory");
             }
         };
         for (int t = 0; t < M; t += 3) {
