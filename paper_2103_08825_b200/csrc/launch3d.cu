@@ -333,7 +333,7 @@ int launch_box3d(sb_plan* P, int src_idx) {
     // CTA is shorter, then guided lengths down to MIN planes -- the last items are short, so
     // the CTAs finish together (equal segments only, SB200_B3_GUIDE=0: 7.8 rounds of items,
     // 6-8% of the SM cycles idle at the end).
-    const double per = env_double("SB200_B3_ITEMS_PER_CTA", 8.0);
+    const double per = env_double("SB200_B3_ITEMS_PER_CTA", 6.0);   // (4-6: fp32 771, fp64 417; 8: 763 / 414; 10-12: 754 / 410)
     const double guide = env_double("SB200_B3_GUIDE", 2.5);
     const int64_t lmin = std::max<int64_t>(1, (int64_t)env_double("SB200_B3_MIN_PLANES", 12));
     const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
@@ -393,13 +393,16 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     // NW=8 (64 x 32, 2/SM) 403-410, 3 CTAs/SM without a register cap 399-409;
     // rejected: 96-thread CTAs (366-377), a skewed pipeline on mbarriers (390-402),
     // per-die work queues (402), a warp-specialised level split (335)
-    static const int nw = (int)env_double("SB200_B3_NW", 4);
+    // (with the guided tail of the z schedule: fp32 3x-unrolled loop 713 -> 761, 64 x 32 tiles
+    // 765; fp64 64 x 32 tiles 411 -> 414)
+    static const int nw = (int)env_double("SB200_B3_NW", 8);
     static const int minb = (int)env_double("SB200_B3_MINB", 0);
     // fp32: with the scalar dx = 0 term (no input-pair moves) the single-copy loop wins
     // (C5 fp32: 713 vs 691 GStencil/s for the 3x-unrolled, role-renamed one; 5 or 6
     // CTAs/SM, SB200_B3_MINB, measured equal: 700-712)
-    static const int u3 = (int)env_double("SB200_B3_U3", 0);
+    static const int u3 = (int)env_double("SB200_B3_U3", 1);
     if constexpr (sizeof(T) == 4 && FMA) {
+        if (u3 && nw == 8 && minb == 3) return launch_box3d<T, FMA, 8, 3, true>(P, src_idx);
         if (u3 && nw == 8) return launch_box3d<T, FMA, 8, 2, true>(P, src_idx);
         if (u3 && minb == 6) return launch_box3d<T, FMA, 4, 6, true>(P, src_idx);
         if (u3 && minb == 5) return launch_box3d<T, FMA, 4, 5, true>(P, src_idx);
