@@ -53,6 +53,8 @@ constexpr int c3_smem_bytes() { return C3_NS * C3Plane<T, NTY>::ELEMS * (int)siz
 // Composed weight of offset (dz, dy, dx) in the 5 x 5 x 5 cube (zero off the diamond).
 __host__ __device__ constexpr int c3_widx(int dz, int dy, int dx) { return (dz + 2) * 25 + (dy + 2) * 5 + (dx + 2); }
 
+constexpr int C3_MAX_SEG = 47;
+
 template <typename T>
 struct Compose3DParams {
     const T* src;
@@ -64,6 +66,7 @@ struct Compose3DParams {
     int x0_first;            // x origin of the first tile (<= 0; TMA box starts 16 B aligned)
     int tiles_x, tiles_y, nseg, lz, items, total_ctas;
     int z0, z1;              // output planes [z0, z1) of this launch (range launches)
+    int zb[C3_MAX_SEG + 1];  // z segment s = [zb[s], zb[s+1]): equal lengths, then a guided tail (launch3d.cu)
     unsigned int* counter;
     T w[125];                // composed weights w[c3_widx(dz, dy, dx)], |dz|+|dy|+|dx| <= 2
     T wx[2][125];            // exact two-step weights of the x = 0 / x = nx-1 face points
@@ -177,7 +180,7 @@ compose3d_kernel(const __grid_constant__ CUtensorMap tmap, const Compose3DParams
         const int hpc = (hs == 0 ? 0 : P.nx - 1) - x0 + 2;                // plane column of the point
         const T* const wf = P.wx[hs];
         T* const obase = P.dst + P.origin + (int64_t)(y0 + 4 * ty) * P.sy + (x0 + 2 * tx);
-        const int zs0 = P.z0 + seg * P.lz, zs1 = min(P.z1, zs0 + P.lz);
+        const int zs0 = P.zb[seg], zs1 = P.zb[seg + 1];
         const int zlo = P.phys_lo ? 1 : 0, zhi = P.phys_hi ? P.nz - 1 : P.nz;   // z shell excluded
         const int p_first = zs0 - 2;
         const int M = (zs1 - zs0) + 4;

@@ -195,6 +195,39 @@ bool compose3d_ok(const sb_plan* P, int k) {
            P->dims[0] >= 4 && P->dims[1] >= 4 && P->dims[2] >= 4;
 }
 
+// z segments of a persistent 2.5D launch, the same for every xy tile (items are claimed
+// tile-fastest, so the CTAs running together work on neighbouring tiles of one z range and
+// share halo lines in L2).  Equal segments (`per` per CTA) until 1/guide of the remaining
+// planes per CTA is shorter, then guided lengths down to `lmin` planes -- the last items
+// are short, so the CTAs finish together (equal segments only, guide = 0: ~7.8 rounds of
+// items on C5, 6-8% of the SM cycles idle at the end).  No segment is longer than the equal
+// split's: long first items let the CTAs drift apart in z and lose the L2 sharing (C5
+// uncapped: fp64 406 -> 393, fp32 704 -> 615 GStencil/s).  Returns the segment count.
+int guided_z_segments(int64_t z_lo, int64_t nzr, int tiles, int ctas_max, double per, double guide, int64_t lmin,
+                      int* zb, int max_seg) {
+    int nb = 0;
+    zb[0] = (int)z_lo;
+    lmin = std::max<int64_t>(1, lmin);
+    const int64_t neq = std::max<int64_t>(1, std::min<int64_t>(max_seg, (int64_t)(per * ctas_max / tiles + 0.5)));
+    const int64_t lmax = std::max<int64_t>(guide > 0 ? lmin : 1, (nzr + neq - 1) / neq);
+    int64_t rem = nzr;
+    while (rem > 0) {
+        int64_t len = lmax;
+        if (guide > 0) {
+            len = (int64_t)std::ceil((double)rem * tiles / (guide * ctas_max));
+            len = std::min(std::max(len, lmin), lmax);
+            if (rem - len < lmin / 2) len = rem;
+        }
+        if (nb == max_seg - 1) len = rem;
+        len = std::min(len, rem);
+        zb[nb + 1] = zb[nb] + (int)len;
+        nb++;
+        rem -= len;
+    }
+    for (int i = nb + 1; i <= max_seg; i++) zb[i] = zb[nb];
+    return nb;
+}
+
 template <typename T, int NTY, int MINB>
 int launch_compose3d(sb_plan* P, int src_idx) {
     constexpr int GEO = NTY == 8 ? 3 : 2;
@@ -232,9 +265,9 @@ int launch_compose3d(sb_plan* P, int src_idx) {
     const int tiles = prm.tiles_x * prm.tiles_y;
     const double per = env_double("SB200_C3_ITEMS_PER_CTA", 12.0);
     const int64_t z_lo = range_lo(P), z_hi = range_hi(P), nzr = z_hi - z_lo;
-    int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(nzr, (int64_t)(per * ctas_max / tiles + 0.5)));
-    prm.lz = (int)((nzr + nseg - 1) / nseg);
-    prm.nseg = (int)((nzr + prm.lz - 1) / prm.lz);
+    prm.lz = 0;
+    prm.nseg = guided_z_segments(z_lo, nzr, tiles, ctas_max, per, env_double("SB200_C3_GUIDE", 0)   /* HBM-bound: the guided tail measured 603 vs 608 */,
+                                 (int64_t)env_double("SB200_C3_MIN_PLANES", 12), prm.zb, sb::C3_MAX_SEG);
     prm.z0 = (int)z_lo;
     prm.z1 = (int)z_hi;
     prm.items = tiles * prm.nseg;
@@ -278,8 +311,10 @@ int launch_compose3d(sb_plan* P, int src_idx) {
     P->kernels_launched++;
 
     P->last_kernel = "compose3d_kernel";
-    kern<<<(unsigned)prm.total_ctas, sb::C3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
-    SB_CUDA(cudaGetLastError());
+    if (prm.items > 0) {
+        kern<<<(unsigned)prm.total_ctas, sb::C3Geo<NTY>::THREADS, smem, P->stream>>>(P->tmap[GEO][src_idx], prm);
+        SB_CUDA(cudaGetLastError());
+    }
     SB_CUDA(cudaStreamWaitEvent(P->stream, P->join_ev, 0));   // join
     return SB_OK;
 }
@@ -327,44 +362,10 @@ int launch_box3d(sb_plan* P, int src_idx) {
     prm.tiles_y = (int)((P->dims[1] + G::TY - 1) / G::TY);
     const int ctas_max = P->num_sms * occ;
     const int tiles = prm.tiles_x * prm.tiles_y;
-    // z segments, the same for every xy tile (items are claimed tile-fastest, so the CTAs
-    // running together work on neighbouring tiles of one z range and share halo lines in
-    // L2).  Equal segments (ITEMS_PER_CTA per CTA) until 1/GUIDE of the remaining planes per
-    // CTA is shorter, then guided lengths down to MIN planes -- the last items are short, so
-    // the CTAs finish together (equal segments only, SB200_B3_GUIDE=0: 7.8 rounds of items,
-    // 6-8% of the SM cycles idle at the end).
     const double per = env_double("SB200_B3_ITEMS_PER_CTA", 6.0);   // (4-6: fp32 771, fp64 417; 8: 763 / 414; 10-12: 754 / 410)
-    const double guide = env_double("SB200_B3_GUIDE", 2.5);
-    const int64_t lmin = std::max<int64_t>(1, (int64_t)env_double("SB200_B3_MIN_PLANES", 12));
     const int64_t z_lo = range_lo(P), nzr = range_hi(P) - z_lo;
-    int nb = 0;
-    prm.zb[0] = (int)z_lo;
-    if (guide > 0) {
-        // no segment longer than the equal split's: long first items let the CTAs drift apart
-        // in z and lose the L2 sharing (uncapped: C5 fp64 406 -> 393, fp32 704 -> 615 GStencil/s)
-        const int64_t neq = std::max<int64_t>(1, (int64_t)(per * ctas_max / tiles + 0.5));
-        const int64_t lmax = std::max<int64_t>(lmin, (nzr + neq - 1) / neq);
-        int64_t rem = nzr;
-        while (rem > 0) {
-            int64_t len = (int64_t)std::ceil((double)rem * tiles / (guide * ctas_max));
-            len = std::min(std::max(len, lmin), lmax);
-            if (nb == sb::B3_MAX_SEG - 1 || rem - len < lmin / 2) len = rem;
-            len = std::min(len, rem);
-            prm.zb[nb + 1] = prm.zb[nb] + (int)len;
-            nb++;
-            rem -= len;
-        }
-    } else {
-        const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(nzr, sb::B3_MAX_SEG),
-                                                                   (int64_t)(per * ctas_max / tiles + 0.5)));
-        const int64_t lz = (nzr + nseg - 1) / nseg;
-        for (int64_t z = 0; z < nzr; z += lz) {
-            prm.zb[nb + 1] = (int)(z_lo + std::min(z + lz, nzr));
-            nb++;
-        }
-    }
-    for (int i = nb + 1; i <= sb::B3_MAX_SEG; i++) prm.zb[i] = prm.zb[nb];
-    prm.nseg = nb;
+    prm.nseg = guided_z_segments(z_lo, nzr, tiles, ctas_max, per, env_double("SB200_B3_GUIDE", 2.5),
+                                 (int64_t)env_double("SB200_B3_MIN_PLANES", 12), prm.zb, sb::B3_MAX_SEG);
     prm.items = tiles * prm.nseg;
     prm.total_ctas = std::min(ctas_max, prm.items);
     prm.counter = P->d_counter;
