@@ -393,7 +393,9 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     // measured (C5, T=100): NW=4 (64 x 16 tiles, 4 CTAs/SM) 402-413 GStencil/s fp64,
     // NW=8 (64 x 32, 2/SM) 403-410, 3 CTAs/SM without a register cap 399-409;
     // rejected: 96-thread CTAs (366-377), a skewed pipeline on mbarriers (390-402),
-    // per-die work queues (402), a warp-specialised level split (335)
+    // per-die work queues (402), a warp-specialised level split (335); fp32: a split-phase
+    // level pipeline (mbarrier arrive after level 1 of plane t, wait before level 2 of plane
+    // t - 1, four level-1 planes: 758 vs 770 -- the CTA barrier is not what bounds it)
     // (with the guided tail of the z schedule: fp32 3x-unrolled loop 713 -> 761, 64 x 32 tiles
     // 765; fp64 64 x 32 tiles 411 -> 414)
     static const int nw = (int)env_double("SB200_B3_NW", 8);
