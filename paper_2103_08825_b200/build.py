@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIB_DIR, "libsb200.so")
-SOURCES = ["sb200.cu", "launch1d.cu", "launch2d.cu", "launch3d.cu", "layout.cu", "multi.cu"]  # compiled in parallel
+SOURCES = ["sb200.cu", "launch1d.cu", "launch2d.cu", "launch3d.cu", "layout.cu", "multi.cu", "hostxfer.cu"]  # compiled in parallel
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

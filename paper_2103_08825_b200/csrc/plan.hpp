@@ -119,6 +119,11 @@ int launch_fused2d(sb_plan* P, int src_idx, int k);
 int launch_fused3d(sb_plan* P, int src_idx, int k);
 int make_tensor_maps(sb_plan* P, int geo, int box_h);
 int finish_upload(sb_plan* P);   // buf[0] uploaded: mirror halo/ghost into buf[1], make buf[0] current
+// hostxfer.cu: transfers for pageable host memory through pinned bounce buffers
+bool host_is_pinned(const void* p);
+int h2d_pageable(void* dst, const void* src, size_t bytes, int device, cudaStream_t st);
+int d2h_pageable_rows(void* host, size_t host_pitch, const void* src, size_t src_pitch, size_t row_bytes, size_t rows,
+                      int device, cudaStream_t st);
 bool sep2d_ok(const sb_plan* P, int k);   // launch2d.cu: separable composed 2D path serves depth k
 inline int64_t range_lo(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_lo : 0; }
 inline int64_t range_hi(const sb_plan* P) { return P->zr_hi >= 0 ? P->zr_hi : P->dims[0]; }

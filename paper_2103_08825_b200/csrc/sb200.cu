@@ -336,7 +336,19 @@ int enqueue_upload(sb_plan* P, const void* host, size_t bytes) {
     SB_CUDA(cudaSetDevice(P->device));
     char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
     static const int staged = (int)env_double("SB200_STAGED_UPLOAD", 1);
-    if (P->d >= 2 && staged) {
+    const bool pinned = host_is_pinned(host);
+    if (!pinned && P->d == 1) {
+        // pageable 1D line: contiguous on both sides, through the pinned bounce buffers
+        const int rc = h2d_pageable(dst, host, bytes, P->device, P->stream);
+        if (rc != SB_OK) return rc;
+    } else if (!pinned) {
+        // pageable box: the contiguous copy into buf[1] through the bounce buffers (hostxfer.cu:
+        // C5 upload 345 -> ~110 ms), then the same device-side re-layout
+        const int rc = h2d_pageable(P->buf[1], host, bytes, P->device, P->stream);
+        if (rc != SB_OK) return rc;
+        SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, P->buf[1], P->host_row_elems * P->es,
+                                  P->host_row_elems * P->es, P->host_rows, cudaMemcpyDeviceToDevice, P->stream));
+    } else if (P->d >= 2 && staged) {
         // Host -> device as ONE contiguous copy into buf[1] (free until the mirror
         // below), then the pitched re-layout device to device: a pitched H2D copy
         // whose destination rows start off the 128 B grid ran at 37.6 GB/s, a
@@ -377,6 +389,21 @@ int enqueue_download(sb_plan* P, void* host, size_t bytes) {
                     (long long)(P->host_elems * (int64_t)P->es));
     SB_CUDA(cudaSetDevice(P->device));
     const char* src = reinterpret_cast<const char*>(P->buf[P->cur]) + P->host_dst_offset * P->es;
+    if (!host_is_pinned(host)) {
+        // pageable destination (a numpy array): chunks through the pinned bounce buffers, copied
+        // out by a few host threads while the next chunk arrives (C5 download 870-1050 -> ~150 ms);
+        // returns with the data in `host`
+        const size_t rb = (size_t)P->host_row_elems * P->es;
+        if (P->host_rows == 1) {                    // one long line: pieces of 4 MB as rows
+            const size_t piece = 4u << 20, full = rb / piece;
+            int rc = d2h_pageable_rows(host, piece, src, piece, piece, full, P->device, P->stream);
+            if (rc == SB_OK && rb > full * piece)
+                rc = d2h_pageable_rows(static_cast<char*>(host) + full * piece, rb - full * piece, src + full * piece,
+                                       rb - full * piece, rb - full * piece, 1, P->device, P->stream);
+            return rc;
+        }
+        return d2h_pageable_rows(host, rb, src, (size_t)P->px * P->es, rb, (size_t)P->host_rows, P->device, P->stream);
+    }
     SB_CUDA(cudaMemcpy2DAsync(host, P->host_row_elems * P->es, src, P->px * P->es,
                               P->host_row_elems * P->es, P->host_rows, cudaMemcpyDeviceToHost, P->stream));
     return SB_OK;

@@ -354,7 +354,16 @@ class MultiPlan:
 
 
 _CACHE = threading.local()
-PLAN_CACHE_SIZE = 8     # plans kept per host thread (device memory stays allocated)
+PLAN_CACHE_SIZE = 8           # plans kept per host thread (device memory stays allocated)
+PLAN_CACHE_BYTES = 24 << 30   # ... and their device memory, least recently used evicted first
+
+
+def _plan_bytes(spec, dims, dtype) -> int:
+    """Device memory of a plan, roughly: two pitched halo-inclusive buffers."""
+    n = 1
+    for a, d in enumerate(dims):
+        n *= int(d) + 2 * spec.r + (32 if a == len(dims) - 1 else 0)
+    return 2 * n * (4 if dtype == "f32" else 8)
 
 
 def cached_plan(spec, dims, *, dtype="f64", arith="fma", k=0, kernel="auto", device=0) -> "Plan":
@@ -378,8 +387,10 @@ def cached_plan(spec, dims, *, dtype="f64", arith="fma", k=0, kernel="auto", dev
         cache.move_to_end(key)
         return p
     p = Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device)
+    p._cache_bytes = _plan_bytes(spec, dims, dtype)
     cache[key] = p
-    while len(cache) > PLAN_CACHE_SIZE:
+    while len(cache) > 1 and (len(cache) > PLAN_CACHE_SIZE or
+                              sum(q._cache_bytes for q in cache.values()) > PLAN_CACHE_BYTES):
         _, old = cache.popitem(last=False)
         old.close()
     return p
@@ -418,6 +429,13 @@ def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
             p.upload(np.ascontiguousarray(box, dtype=np_dtype))
             p.run(steps)
             return p.download()
+    if _plan_bytes(spec, dims, dtype) <= PLAN_CACHE_BYTES // 2:
+        # the calling thread's cached plan: creating and freeing the two grid buffers costs
+        # 10-550 ms around a 100 ms sweep (C5); clear_plan_cache() releases the memory
+        p = cached_plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device)
+        p.upload(np.ascontiguousarray(box, dtype=np_dtype))
+        p.run(steps)
+        return p.download()
     with Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device) as p:
         p.upload(np.ascontiguousarray(box, dtype=np_dtype))
         p.run(steps)
