@@ -116,6 +116,17 @@ int sb_upload(sb_plan *plan, const void *host, size_t bytes);
 /* Device (current buffer) -> host box, halo included. */
 int sb_download(sb_plan *plan, void *host, size_t bytes);
 
+/* The same with the host box given as uniformly pitched rows: row i of the box
+ * (sb_host_elems / row-elements rows, slowest axes first) starts at
+ * host + i * pitch_bytes, pitch_bytes >= the row's bytes.  A NATURAL
+ * GridBuffer.data (stencilbench/core.py:232-373) whose halo equals the stencil
+ * order is such a box -- first row at &data[..., halo_unit - r], pitch = one
+ * storage row -- so b200_sweep moves it without a compacting host copy;
+ * sb_download_pitched writes the box's rows back (the halo cells get the values
+ * they already hold, cells outside the box are not touched). */
+int sb_upload_pitched(sb_plan *plan, const void *host, size_t pitch_bytes);
+int sb_download_pitched(sb_plan *plan, void *host, size_t pitch_bytes);
+
 /* Stream-ordered forms of sb_upload / sb_download on the plan stream: they
  * return once the copy is enqueued.  `host` must stay valid (and should be
  * page-locked, e.g. cudaHostAlloc, for the copy to overlap other work) until

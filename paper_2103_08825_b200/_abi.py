@@ -26,7 +26,8 @@ EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
            "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
            "sb_multi_create", "sb_multi_destroy", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
-           "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times")
+           "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times",
+           "sb_upload_pitched", "sb_download_pitched")
 
 
 class SbProblem(ctypes.Structure):
@@ -76,6 +77,8 @@ def load():
     lib.sb_upload.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_download.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_upload_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
+    lib.sb_upload_pitched.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
+    lib.sb_download_pitched.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_download_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_synchronize.argtypes = [P]
     lib.sb_step_box.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -114,7 +117,8 @@ def load():
                  "sb_upload_async", "sb_download_async", "sb_synchronize", "sb_step_box",
                  "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
                  "sb_multi_create", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
-                 "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times"):
+                 "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times",
+           "sb_upload_pitched", "sb_download_pitched"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

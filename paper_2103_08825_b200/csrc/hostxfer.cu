@@ -94,26 +94,41 @@ bool host_is_pinned(const void* p) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
-// Contiguous pageable host -> device, stream-ordered on `st`; returns when the last
-// chunk has been handed to the copy engine out of a bounce buffer (the caller's array is
-// no longer read).
-int h2d_pageable(void* dst, const void* src, size_t bytes, int device, cudaStream_t st) {
+// Pageable host rows (pitch host_pitch) -> contiguous device rows, stream-ordered on `st`;
+// returns when the last chunk has been handed to the copy engine out of a bounce buffer
+// (the caller's array is no longer read).
+int h2d_pageable_rows(void* dst, const void* host, size_t host_pitch, size_t row_bytes, size_t rows, int device,
+                      cudaStream_t st) {
     std::lock_guard<std::mutex> lock(g_bounce.mu);
     const int rc = bounce_ready(device);
     if (rc != SB_OK) return rc;
     Bounce& b = g_bounce;
+    if (row_bytes > kChunk) return fail(SB_ERR_ARG, "row of %zu bytes exceeds the transfer chunk", row_bytes);
+    const size_t rpc = std::max<size_t>(1, kChunk / row_bytes);   // rows per chunk
     int slot = 0;
-    for (size_t off = 0; off < bytes; off += kChunk, slot ^= 1) {
-        const size_t n = std::min(kChunk, bytes - off);
+    for (size_t r0 = 0; r0 < rows; r0 += rpc, slot ^= 1) {
+        const size_t nr = std::min(rpc, rows - r0);
         SB_CUDA(cudaEventSynchronize(b.ev[slot]));      // the copy that last read this buffer is done
-        parallel_copy_rows(static_cast<char*>(b.buf[slot]), n, static_cast<const char*>(src) + off, n, n, 1);
-        SB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, b.buf[slot], n, cudaMemcpyHostToDevice, st));
+        parallel_copy_rows(static_cast<char*>(b.buf[slot]), row_bytes, static_cast<const char*>(host) + r0 * host_pitch,
+                           host_pitch, row_bytes, nr);
+        SB_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + r0 * row_bytes, b.buf[slot], nr * row_bytes,
+                                cudaMemcpyHostToDevice, st));
         SB_CUDA(cudaEventRecord(b.ev[slot], st));
     }
     // the bounce buffers are shared: the next transfer may overwrite them
     SB_CUDA(cudaEventSynchronize(b.ev[0]));
     SB_CUDA(cudaEventSynchronize(b.ev[1]));
     return SB_OK;
+}
+
+// Contiguous pageable bytes: pieces of 4 MB as rows, then the remainder.
+int h2d_pageable(void* dst, const void* src, size_t bytes, int device, cudaStream_t st) {
+    const size_t piece = 4u << 20, full = bytes / piece;
+    int rc = h2d_pageable_rows(dst, src, piece, piece, full, device, st);
+    if (rc == SB_OK && bytes > full * piece)
+        rc = h2d_pageable_rows(static_cast<char*>(dst) + full * piece, static_cast<const char*>(src) + full * piece,
+                               bytes - full * piece, bytes - full * piece, 1, device, st);
+    return rc;
 }
 
 // Pitched device rows -> compact pageable host rows; returns when `host` holds the data.

@@ -122,6 +122,8 @@ int finish_upload(sb_plan* P);   // buf[0] uploaded: mirror halo/ghost into buf[
 // hostxfer.cu: transfers for pageable host memory through pinned bounce buffers
 bool host_is_pinned(const void* p);
 int h2d_pageable(void* dst, const void* src, size_t bytes, int device, cudaStream_t st);
+int h2d_pageable_rows(void* dst, const void* host, size_t host_pitch, size_t row_bytes, size_t rows, int device,
+                      cudaStream_t st);
 int d2h_pageable_rows(void* host, size_t host_pitch, const void* src, size_t src_pitch, size_t row_bytes, size_t rows,
                       int device, cudaStream_t st);
 bool sep2d_ok(const sb_plan* P, int k);   // launch2d.cu: separable composed 2D path serves depth k

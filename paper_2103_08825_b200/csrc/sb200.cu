@@ -328,6 +328,42 @@ namespace sbh {
 // Host box -> buf[0], then the halo/ghost into buf[1] too (kernels never
 // write it).  1D copies only the two ends (pad + halo); 2D/3D copy the whole
 // buffer (cheap next to those sweeps).  Stream-ordered, no host sync.
+int enqueue_upload(sb_plan* P, const void* host, size_t bytes);
+int enqueue_download(sb_plan* P, void* host, size_t bytes);
+
+// The host box as uniformly pitched rows (pitch >= the row's bytes): a NATURAL
+// GridBuffer.data whose halo equals the stencil order (core.py:232-373) is one.
+int enqueue_upload_pitched(sb_plan* P, const void* host, size_t pitch) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    const size_t rb = (size_t)P->host_row_elems * P->es;
+    if (pitch < rb) return fail(SB_ERR_GRID, "host pitch %zu below the row size %zu", pitch, rb);
+    if (pitch == rb || P->host_rows == 1) return enqueue_upload(P, host, (size_t)P->host_elems * P->es);
+    SB_CUDA(cudaSetDevice(P->device));
+    char* dst = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
+    if (host_is_pinned(host)) {
+        SB_CUDA(cudaMemcpy2DAsync(P->buf[1], rb, host, pitch, rb, P->host_rows, cudaMemcpyHostToDevice, P->stream));
+    } else {
+        const int rc = h2d_pageable_rows(P->buf[1], host, pitch, rb, (size_t)P->host_rows, P->device, P->stream);
+        if (rc != SB_OK) return rc;
+    }
+    SB_CUDA(cudaMemcpy2DAsync(dst, P->px * P->es, P->buf[1], rb, rb, P->host_rows, cudaMemcpyDeviceToDevice, P->stream));
+    return finish_upload(P);
+}
+
+int enqueue_download_pitched(sb_plan* P, void* host, size_t pitch) {
+    if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
+    if (!P->uploaded) return fail(SB_ERR_STATE, "download before upload");
+    const size_t rb = (size_t)P->host_row_elems * P->es;
+    if (pitch < rb) return fail(SB_ERR_GRID, "host pitch %zu below the row size %zu", pitch, rb);
+    if (pitch == rb || P->host_rows == 1) return enqueue_download(P, host, (size_t)P->host_elems * P->es);
+    SB_CUDA(cudaSetDevice(P->device));
+    const char* src = reinterpret_cast<const char*>(P->buf[P->cur]) + P->host_dst_offset * P->es;
+    if (!host_is_pinned(host))
+        return d2h_pageable_rows(host, pitch, src, (size_t)P->px * P->es, rb, (size_t)P->host_rows, P->device, P->stream);
+    SB_CUDA(cudaMemcpy2DAsync(host, pitch, src, P->px * P->es, rb, P->host_rows, cudaMemcpyDeviceToHost, P->stream));
+    return SB_OK;
+}
+
 int enqueue_upload(sb_plan* P, const void* host, size_t bytes) {
     if (!P || !host) return fail(SB_ERR_ARG, "NULL argument");
     if (bytes != (size_t)P->host_elems * P->es)
@@ -646,6 +682,20 @@ int sb_upload(sb_plan* P, const void* host, size_t bytes) {
 
 int sb_download(sb_plan* P, void* host, size_t bytes) {
     const int rc = sbh::enqueue_download(P, host, bytes);
+    if (rc != SB_OK) return rc;
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
+}
+
+int sb_upload_pitched(sb_plan* P, const void* host, size_t pitch_bytes) {
+    const int rc = sbh::enqueue_upload_pitched(P, host, pitch_bytes);
+    if (rc != SB_OK) return rc;
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    return SB_OK;
+}
+
+int sb_download_pitched(sb_plan* P, void* host, size_t pitch_bytes) {
+    const int rc = sbh::enqueue_download_pitched(P, host, pitch_bytes);
     if (rc != SB_OK) return rc;
     SB_CUDA(cudaStreamSynchronize(P->stream));
     return SB_OK;

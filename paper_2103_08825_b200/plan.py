@@ -136,6 +136,15 @@ class Plan:
         _abi.check(self._lib.sb_download(self._h, out.ctypes.data, out.nbytes))
         return out
 
+    def upload_pitched(self, first_row: int, pitch_bytes: int) -> None:
+        """Upload a host box given as uniformly pitched rows (``first_row``: address
+        of row 0; see ``sb_upload_pitched``) -- a NATURAL GridBuffer in place."""
+        _abi.check(self._lib.sb_upload_pitched(self._h, ctypes.c_void_p(first_row), int(pitch_bytes)))
+
+    def download_pitched(self, first_row: int, pitch_bytes: int) -> None:
+        """Write the current box back into pitched host rows (``sb_download_pitched``)."""
+        _abi.check(self._lib.sb_download_pitched(self._h, ctypes.c_void_p(first_row), int(pitch_bytes)))
+
     def upload_async(self, box: np.ndarray) -> None:
         """Stream-ordered upload: returns once enqueued; `box` (ideally pinned
         memory) must stay alive and unmodified until :meth:`synchronize`."""

@@ -169,3 +169,26 @@ def test_reference_gridbuffer_if_importable():
     scalar_step(a, b, spec)
     b200_step(a, b2, spec)
     assert np.array_equal(b.natural_interior(), b2.natural_interior())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("cfg,dims,k,T", [("c3b", (130, 300), 4, 9), ("c5", (20, 30, 70), 2, 5),
+                                          ("c4", (17, 33, 129), 2, 6)])
+def test_sweep_natural_grid_in_place_pitched(cfg, dims, k, T):
+    # a NATURAL GridBuffer is uploaded / written back in place as pitched rows
+    # (sb_upload_pitched / sb_download_pitched): every cell of the storage array is seeded,
+    # the compact box (halo held at its values) must equal the oracle's bit for bit and the
+    # cells outside it (the unit axis' extra halo, core.py:335-362) must not be touched
+    spec = config_spec(cfg)
+    g = alloc_grid(spec, dims)
+    g.data[...] = np.random.default_rng(int(np.prod(dims))).random(g.data.shape)
+    snap = g.data.copy()
+    before = np.array(compact_view(g), copy=True)
+    b200_sweep(g, spec, k, T, arith="exact")
+    offs, ws = canonical(spec)
+    want = c_oracle.sweep(before, spec.r, offs, ws, T)
+    assert np.array_equal(compact_view(g), want)
+    outside = np.ones(g.data.shape, bool)
+    hu, r = g.halo_unit, spec.r
+    outside[..., hu - r:hu + g.unit_n + r] = False
+    assert np.array_equal(g.data[outside], snap[outside])
