@@ -111,7 +111,12 @@ def b200_step(src, dst, spec, counters=None, ranges=None, *, arith="exact") -> N
         raise GridError(f"{layout_value(src)} grid sized for order {src.r}, stencil order {r}")
     kernel = "generic" if ranges is not None else "auto"
     p = cached_plan(spec, tuple(src.dims), arith=arith, k=1, kernel=kernel)
-    if natural:
+    sd = src.data
+    if (natural and src.r == r and sd.dtype == np.float64 and sd.flags.c_contiguous and sd.ndim >= 2):
+        # the storage array is the host box with a row pitch: no compacting copy (see b200_sweep);
+        # dst takes only its interior below (its own halo stays, kernels.py:120-134)
+        p.upload_pitched(sd.ctypes.data + (src.halo_unit - r) * sd.itemsize, sd.shape[-1] * sd.itemsize)
+    elif natural:
         p.upload(np.ascontiguousarray(compact_view(src, r), dtype=np.float64))
     else:
         p.upload_storage(src)
