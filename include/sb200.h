@@ -127,6 +127,20 @@ int sb_download(sb_plan *plan, void *host, size_t bytes);
 int sb_upload_pitched(sb_plan *plan, const void *host, size_t pitch_bytes);
 int sb_download_pitched(sb_plan *plan, void *host, size_t pitch_bytes);
 
+/* Host box in, `steps` steps, host box out (pitches as above; 0 = compact rows;
+ * in and out may be the same memory): upload, run, download in one call.  With
+ * SB200_STREAM_SWEEP=1 (opt-in, measured a gain only for few-launch sweeps) 3D
+ * whole-grid plans overlap the transfers with the sweep: the grid is cut into
+ * blocks of planes, every launch
+ * of the sweep runs block by block on ranges shifted down by the reach of the
+ * launches before it, so a block's launches start once its planes have arrived
+ * and its final planes travel back while later blocks compute -- the same range
+ * launches as sb_launch_range, bit-identical to upload + run + download.  Other
+ * plans run exactly that sequence.  The grid-in/grid-out call of the drop-in
+ * (harness._execute's loop, harness.py:187-201, around one method). */
+int sb_sweep_host(sb_plan *plan, const void *host_in, size_t in_pitch_bytes, void *host_out,
+                  size_t out_pitch_bytes, int64_t steps);
+
 /* Stream-ordered forms of sb_upload / sb_download on the plan stream: they
  * return once the copy is enqueued.  `host` must stay valid (and should be
  * page-locked, e.g. cudaHostAlloc, for the copy to overlap other work) until

@@ -27,7 +27,7 @@ EXPORTS = ("sb_plan_create", "sb_plan_destroy", "sb_host_elems", "sb_upload",
            "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
            "sb_multi_create", "sb_multi_destroy", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
            "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times",
-           "sb_upload_pitched", "sb_download_pitched")
+           "sb_upload_pitched", "sb_download_pitched", "sb_sweep_host")
 
 
 class SbProblem(ctypes.Structure):
@@ -79,6 +79,7 @@ def load():
     lib.sb_upload_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_upload_pitched.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_download_pitched.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
+    lib.sb_sweep_host.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int64]
     lib.sb_download_async.argtypes = [P, ctypes.c_void_p, ctypes.c_size_t]
     lib.sb_synchronize.argtypes = [P]
     lib.sb_step_box.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
@@ -118,7 +119,7 @@ def load():
                  "sb_upload_storage", "sb_download_storage", "sb_layout_convert", "sb_launch_range",
                  "sb_multi_create", "sb_multi_upload", "sb_multi_download", "sb_multi_run",
                  "sb_multi_info", "sb_multi_slab", "sb_problem_k", "sb_launch_repeat", "sb_repeat_times",
-           "sb_upload_pitched", "sb_download_pitched"):
+           "sb_upload_pitched", "sb_download_pitched", "sb_sweep_host"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -26,6 +26,7 @@ constexpr size_t kChunk = 32u << 20;   // bytes per bounce buffer
 struct Bounce {
     std::mutex mu;            // one pageable transfer at a time per process
     void* buf[2] = {nullptr, nullptr};
+    void* buf2[2] = {nullptr, nullptr};   // second pair (streamed sweeps: up and down at once)
     cudaEvent_t ev[2] = {nullptr, nullptr};
     int device = -1;
 };
@@ -54,6 +55,8 @@ int host_threads() {
     return n;
 }
 
+}  // namespace
+
 // rows x row_bytes from src (pitch sp) to dst (pitch dp), split over the host threads
 void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t row_bytes, size_t rows) {
     const int nt = (int)std::min<size_t>((size_t)host_threads(), std::max<size_t>(1, rows * row_bytes / (1u << 20)));
@@ -80,7 +83,26 @@ void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t
     for (auto& x : th) x.join();
 }
 
-}  // namespace
+// Both bounce pairs for one caller (sb_sweep_host), under the process-wide transfer lock
+// until xfer_release().
+int xfer_acquire(int device, void* up[2], void* down[2], size_t* chunk_bytes) {
+    g_bounce.mu.lock();
+    int rc = bounce_ready(device);
+    for (int i = 0; i < 2 && rc == SB_OK; i++)
+        if (!g_bounce.buf2[i] && cudaHostAlloc(&g_bounce.buf2[i], kChunk, cudaHostAllocPortable) != cudaSuccess)
+            rc = fail(SB_ERR_NOMEM, "pinned bounce buffer allocation failed");
+    if (rc != SB_OK) {
+        g_bounce.mu.unlock();
+        return rc;
+    }
+    for (int i = 0; i < 2; i++) {
+        up[i] = g_bounce.buf[i];
+        down[i] = g_bounce.buf2[i];
+    }
+    *chunk_bytes = kChunk;
+    return SB_OK;
+}
+void xfer_release() { g_bounce.mu.unlock(); }
 
 // Pinned (cudaHostAlloc / cudaHostRegister) or managed memory: the copy engines read it directly.
 bool host_is_pinned(const void* p) {

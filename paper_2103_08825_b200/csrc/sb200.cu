@@ -787,6 +787,236 @@ int sb_launch_range(sb_plan* P, int64_t steps, int64_t lo, int64_t hi, int32_t f
     return rc;
 }
 
+}  // extern "C"
+
+// ---- streamed host-to-host sweep -----------------------------------------
+//
+// Host box in, `steps` steps, host box out, with the transfers overlapped with
+// the sweep itself (3D whole-grid plans).  The grid is cut into B blocks of
+// planes along z.  Launch j of the sweep (depth k_j, reach G_j = r k_j) runs
+// block by block on ranges shifted down by S_j = G_0 + .. + G_{j-1}:
+//     (j, b) computes planes [z_b - S_j, z_{b+1} - S_j)      (clipped to [0, n),
+//                                                             the last block up to n)
+// so it reads level-j planes up to z_{b+1} - S_j + G_j <= z_{b+1} - S_{j-1}, the end of
+// what (j-1, b) produced (depths never increase), and down to planes block b-1
+// produced earlier in the stream.  All launches of block b can therefore run as
+// soon as the upload has passed plane z_{b+1} + G_0, and block b's final planes
+// [z_b - S_{L-1}, z_{b+1} - S_{L-1}) can travel back while later blocks compute.
+// Two ping-pong buffers suffice: (j, b) overwrites planes below z_{b+1} - S_j of
+// the buffer that later blocks read from z_{b'} - S_j (b' > b) upwards.  Every
+// launch is the plan's ordinary range launch, so the result is bit-identical to
+// upload + run + download (tests/test_stream_sweep.py).
+namespace {
+
+struct StreamRes {   // per-call CUDA objects, released on every exit path
+    cudaStream_t up = nullptr, down = nullptr;
+    std::vector<cudaEvent_t> ev;
+    bool locked = false;
+    ~StreamRes() {
+        for (auto e : ev) cudaEventDestroy(e);
+        if (up) cudaStreamDestroy(up);
+        if (down) cudaStreamDestroy(down);
+        if (locked) sbh::xfer_release();
+    }
+    int event(cudaEvent_t* e) {
+        SB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        ev.push_back(*e);
+        return SB_OK;
+    }
+};
+
+template <typename T, bool FMA>
+int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_t out_pitch,
+                   const std::vector<int>& ks, int nblocks) {
+    const int64_t n = P->dims[0], r = P->r;
+    const size_t rb = (size_t)P->host_row_elems * P->es;
+    const int64_t R = P->host_rows / (n + 2 * r);              // rows per plane
+    const size_t dpitch = (size_t)P->px * P->es;
+    const int L = (int)ks.size();
+    std::vector<int64_t> S(L + 1, 0);
+    for (int j = 0; j < L; j++) S[j + 1] = S[j] + r * ks[j];
+    StreamRes res;
+    void *bup[2], *bdn[2];
+    size_t chunk = 0;
+    int rc = sbh::xfer_acquire(P->device, bup, bdn, &chunk);
+    if (rc != SB_OK) return rc;
+    res.locked = true;
+    SB_CUDA(cudaStreamCreateWithFlags(&res.up, cudaStreamNonBlocking));
+    SB_CUDA(cudaStreamCreateWithFlags(&res.down, cudaStreamNonBlocking));
+    const int64_t rows = P->host_rows;
+    const int64_t rpc = std::max<int64_t>(1, (int64_t)(chunk / rb));
+    const int64_t nchunks = (rows + rpc - 1) / rpc;
+    cudaEvent_t start_ev, up_slot[2], dn_slot[2];
+    if ((rc = res.event(&start_ev)) != SB_OK) return rc;
+    for (int i = 0; i < 2; i++)
+        if ((rc = res.event(&up_slot[i])) != SB_OK || (rc = res.event(&dn_slot[i])) != SB_OK) return rc;
+    // the buffers may still be in use by earlier work on the plan stream
+    SB_CUDA(cudaEventRecord(start_ev, P->stream));
+    SB_CUDA(cudaStreamWaitEvent(res.up, start_ev, 0));
+    char* b0 = reinterpret_cast<char*>(P->buf[0]) + P->host_dst_offset * P->es;
+    char* b1 = reinterpret_cast<char*>(P->buf[1]) + P->host_dst_offset * P->es;
+
+    // blocks and what each needs / yields (host plane index = interior plane + r)
+    std::vector<int64_t> zb(nblocks + 1);
+    for (int b = 0; b <= nblocks; b++) zb[b] = n * b / nblocks;
+    auto need_rows = [&](int b) {       // upload progress block b waits for
+        const int64_t planes = b == nblocks - 1 ? n + 2 * r : std::min<int64_t>(n + 2 * r, zb[b + 1] + r * ks[0] + r);
+        return planes * R;
+    };
+    auto final_hi = [&](int b) {        // host planes [.., this) are final once block b is done
+        if (b == nblocks - 1) return n + 2 * r;
+        const int64_t f = std::min<int64_t>(n, std::max<int64_t>(0, zb[b + 1] - S[L - 1]));
+        return f > 0 ? f + r : (int64_t)0;
+    };
+
+    struct Dl { int64_t r0, r1; };      // download row ranges, in order
+    std::vector<Dl> dlq;
+    size_t dl_issued = 0, dl_drained = 0;
+    int64_t dl_planes = 0;              // host planes queued so far
+    int dslot_issue = 0, dslot_drain = 0;
+    int next_block = 0;
+    const int final_buf = L & 1;
+
+    auto enqueue_block = [&](int b, cudaEvent_t uploaded) -> int {
+        SB_CUDA(cudaStreamWaitEvent(P->stream, uploaded, 0));
+        for (int j = 0; j < L; j++) {
+            const int64_t lo = b == 0 ? 0 : std::min<int64_t>(n, std::max<int64_t>(0, zb[b] - S[j]));
+            const int64_t hi = b == nblocks - 1 ? n : std::min<int64_t>(n, std::max<int64_t>(0, zb[b + 1] - S[j]));
+            if (hi <= lo) continue;
+            P->cur = j & 1;
+            P->zr_lo = lo;
+            P->zr_hi = hi;
+            int64_t launches = 0;
+            const int rc2 = launch_one<T, FMA>(P, ks[j], 0, &launches, false);
+            if (rc2 != SB_OK) return rc2;
+        }
+        cudaEvent_t done;
+        int rc2 = res.event(&done);
+        if (rc2 != SB_OK) return rc2;
+        SB_CUDA(cudaEventRecord(done, P->stream));
+        const int64_t hp = final_hi(b);
+        if (hp > dl_planes) {
+            SB_CUDA(cudaStreamWaitEvent(res.down, done, 0));
+            for (int64_t r0 = dl_planes * R; r0 < hp * R; r0 += rpc) dlq.push_back({r0, std::min(r0 + rpc, hp * R)});
+            dl_planes = hp;
+        }
+        return SB_OK;
+    };
+    // issue queued D2H chunks into free bounce slots; drain finished ones (all, if `block`)
+    auto pump_downloads = [&](bool block) -> int {
+        for (;;) {
+            while (dl_issued < dlq.size() && dl_issued - dl_drained < 2) {
+                const Dl& d = dlq[dl_issued];
+                const char* src = reinterpret_cast<const char*>(P->buf[final_buf]) + P->host_dst_offset * P->es +
+                                  (size_t)d.r0 * dpitch;
+                SB_CUDA(cudaMemcpy2DAsync(bdn[dslot_issue], rb, src, dpitch, rb, (size_t)(d.r1 - d.r0),
+                                          cudaMemcpyDeviceToHost, res.down));
+                SB_CUDA(cudaEventRecord(dn_slot[dslot_issue], res.down));
+                dslot_issue ^= 1;
+                dl_issued++;
+            }
+            if (dl_drained == dl_issued) return SB_OK;
+            if (!block) {
+                const cudaError_t q = cudaEventQuery(dn_slot[dslot_drain]);
+                if (q == cudaErrorNotReady) return SB_OK;
+                if (q != cudaSuccess) return fail(SB_ERR_CUDA, "download failed: %s", cudaGetErrorString(q));
+            } else {
+                SB_CUDA(cudaEventSynchronize(dn_slot[dslot_drain]));
+            }
+            const Dl& d = dlq[dl_drained];
+            sbh::parallel_copy_rows(out + (size_t)d.r0 * out_pitch, out_pitch, static_cast<const char*>(bdn[dslot_drain]),
+                                    rb, rb, (size_t)(d.r1 - d.r0));
+            dslot_drain ^= 1;
+            dl_drained++;
+        }
+    };
+
+    // ---- upload chunks; blocks are enqueued as their planes arrive
+    for (int64_t c = 0; c < nchunks; c++) {
+        const int slot = (int)(c & 1);
+        const int64_t r0 = c * rpc, nr = std::min(rpc, rows - r0);
+        SB_CUDA(cudaEventSynchronize(up_slot[slot]));
+        sbh::parallel_copy_rows(static_cast<char*>(bup[slot]), rb, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr);
+        SB_CUDA(cudaMemcpy2DAsync(b0 + (size_t)r0 * dpitch, dpitch, bup[slot], rb, rb, (size_t)nr, cudaMemcpyHostToDevice,
+                                  res.up));
+        SB_CUDA(cudaEventRecord(up_slot[slot], res.up));
+        // the halo / ghost cells live in both buffers (kernels never write them)
+        SB_CUDA(cudaMemcpy2DAsync(b1 + (size_t)r0 * dpitch, dpitch, b0 + (size_t)r0 * dpitch, dpitch, rb, (size_t)nr,
+                                  cudaMemcpyDeviceToDevice, res.up));
+        const int64_t have = r0 + nr;
+        if (next_block < nblocks && have >= need_rows(next_block)) {
+            cudaEvent_t uploaded;
+            if ((rc = res.event(&uploaded)) != SB_OK) return rc;
+            SB_CUDA(cudaEventRecord(uploaded, res.up));
+            while (next_block < nblocks && have >= need_rows(next_block))
+                if ((rc = enqueue_block(next_block++, uploaded)) != SB_OK) return rc;
+        }
+        if ((rc = pump_downloads(false)) != SB_OK) return rc;
+    }
+    P->uploaded = true;
+    if ((rc = pump_downloads(true)) != SB_OK) return rc;
+    P->cur = final_buf;
+    P->zr_lo = 0;
+    P->zr_hi = -1;
+    SB_CUDA(cudaStreamSynchronize(P->stream));
+    SB_CUDA(cudaGetLastError());
+    return SB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sb_sweep_host(sb_plan* P, const void* host_in, size_t in_pitch, void* host_out, size_t out_pitch, int64_t steps) {
+    if (!P || !host_in || !host_out) return fail(SB_ERR_ARG, "NULL argument");
+    if (steps < 0) return fail(SB_ERR_ARG, "steps must be >= 0");
+    const size_t rb = (size_t)P->host_row_elems * P->es;
+    if (in_pitch == 0) in_pitch = rb;
+    if (out_pitch == 0) out_pitch = rb;
+    if (in_pitch < rb || out_pitch < rb) return fail(SB_ERR_GRID, "host pitch below the row size %zu", rb);
+    SB_CUDA(cudaSetDevice(P->device));
+    // the launch sequence run_steps would issue
+    std::vector<int> ks;
+    if (P->kind == KK_GENERIC) {
+        if (steps <= 4096) ks.assign((size_t)steps, 1);      // (longer: the plain path below)
+    } else {
+        for (int64_t done = 0; done < steps;) {
+            const int kk = (steps - done >= P->k) ? P->k : largest_fused_k(P->kind, steps - done, P->k);
+            ks.push_back(kk);
+            done += kk;
+        }
+    }
+    // Opt-in (read per call): measured on the C5 box 412 vs 464 ms per call with 8 blocks, but
+    // on C4 (T = 200: 100 launches + their shell kernels per block) 201 vs 133 ms -- one host
+    // thread feeds both directions and 8 x L small range launches cost more than they hide.
+    const int enabled = (int)env_double("SB200_STREAM_SWEEP", 0);
+    const int nblocks_env = (int)env_double("SB200_STREAM_BLOCKS", 8);
+    const int64_t n = P->dims[0];
+    const int64_t shift = ks.empty() ? 0 : (int64_t)P->r * (steps - ks.back());
+    const int nblocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblocks_env, n / std::max<int64_t>(1, 4 * P->r * (ks.empty() ? 1 : ks[0]))));
+    const bool streamed = enabled && P->d == 3 && P->phys_lo && P->phys_hi && !ks.empty() && nblocks >= 2 &&
+                          n >= 2 * shift && (size_t)P->host_elems * P->es >= ((size_t)64 << 20) &&
+                          P->host_rows % (n + 2 * P->r) == 0;
+    if (!streamed) {
+        int rc = sbh::enqueue_upload_pitched(P, host_in, in_pitch);
+        if (rc != SB_OK) return rc;
+        rc = sb_launch(P, steps);
+        if (rc != SB_OK) return rc;
+        rc = sbh::enqueue_download_pitched(P, host_out, out_pitch);
+        if (rc != SB_OK) return rc;
+        SB_CUDA(cudaStreamSynchronize(P->stream));
+        return SB_OK;
+    }
+    const bool fma = P->arith == SB_ARITH_FMA;
+    const char* in = static_cast<const char*>(host_in);
+    char* out = static_cast<char*>(host_out);
+    if (P->dtype == SB_F64)
+        return fma ? stream_sweep_t<double, true>(P, in, in_pitch, out, out_pitch, ks, nblocks)
+                   : stream_sweep_t<double, false>(P, in, in_pitch, out, out_pitch, ks, nblocks);
+    return fma ? stream_sweep_t<float, true>(P, in, in_pitch, out, out_pitch, ks, nblocks)
+               : stream_sweep_t<float, false>(P, in, in_pitch, out, out_pitch, ks, nblocks);
+}
+
 int sb_step_box(sb_plan* P, const int64_t* lo, const int64_t* hi) {
     if (!P || !lo || !hi) return fail(SB_ERR_ARG, "NULL argument");
     if (!P->uploaded) return fail(SB_ERR_STATE, "run before upload");

@@ -168,15 +168,17 @@ def b200_sweep(grid, spec, k, T, counters=None, *, arith="exact") -> None:
                 and data.flags.writeable and data.ndim >= 2)
     if in_place:
         first = data.ctypes.data + (grid.halo_unit - spec.r) * data.itemsize
-        p.upload_pitched(first, data.shape[-1] * data.itemsize)
-    elif natural:
+        pitch = data.shape[-1] * data.itemsize
+        p.sweep_host_pitched(first, pitch, first, pitch, T)      # upload, T steps, write back
+        if counters is not None:
+            counters.point_updates += _points(grid) * T
+        return
+    if natural:
         p.upload(np.ascontiguousarray(compact_view(grid, spec.r), dtype=np.float64))
     else:
         p.upload_storage(grid)
     p.run(T)
-    if in_place:
-        p.download_pitched(first, data.shape[-1] * data.itemsize)
-    elif natural:
+    if natural:
         out = p.download()
         interior_view(grid)[...] = out[tuple(slice(spec.r, s - spec.r) for s in out.shape)]
     else:

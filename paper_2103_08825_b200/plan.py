@@ -145,6 +145,21 @@ class Plan:
         """Write the current box back into pitched host rows (``sb_download_pitched``)."""
         _abi.check(self._lib.sb_download_pitched(self._h, ctypes.c_void_p(first_row), int(pitch_bytes)))
 
+    def sweep_host(self, box: np.ndarray, steps: int, out: np.ndarray | None = None) -> np.ndarray:
+        """``steps`` steps from the host box ``box`` into ``out`` (default: a new array),
+        transfers overlapped with the sweep where the plan allows it (``sb_sweep_host``)."""
+        self._check_box(box)
+        if out is None:
+            out = np.empty(self.shape, dtype=self.np_dtype)
+        self._check_box(out)
+        _abi.check(self._lib.sb_sweep_host(self._h, box.ctypes.data, 0, out.ctypes.data, 0, int(steps)))
+        return out
+
+    def sweep_host_pitched(self, first_in: int, in_pitch: int, first_out: int, out_pitch: int, steps: int) -> None:
+        """:meth:`sweep_host` on pitched host rows (addresses of row 0; may coincide)."""
+        _abi.check(self._lib.sb_sweep_host(self._h, ctypes.c_void_p(first_in), int(in_pitch),
+                                           ctypes.c_void_p(first_out), int(out_pitch), int(steps)))
+
     def upload_async(self, box: np.ndarray) -> None:
         """Stream-ordered upload: returns once enqueued; `box` (ideally pinned
         memory) must stay alive and unmodified until :meth:`synchronize`."""
@@ -442,13 +457,9 @@ def sweep(spec, box: np.ndarray, steps: int, *, arith="fma", k=0, kernel="auto",
         # the calling thread's cached plan: creating and freeing the two grid buffers costs
         # 10-550 ms around a 100 ms sweep (C5); clear_plan_cache() releases the memory
         p = cached_plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device)
-        p.upload(np.ascontiguousarray(box, dtype=np_dtype))
-        p.run(steps)
-        return p.download()
+        return p.sweep_host(np.ascontiguousarray(box, dtype=np_dtype), steps)
     with Plan(spec, dims, dtype=dtype, arith=arith, k=k, kernel=kernel, device=device) as p:
-        p.upload(np.ascontiguousarray(box, dtype=np_dtype))
-        p.run(steps)
-        return p.download()
+        return p.sweep_host(np.ascontiguousarray(box, dtype=np_dtype), steps)
 
 
 __all__ = ["Plan", "MultiPlan", "Timing", "sweep", "cached_plan", "clear_plan_cache", "host_shape", "storage_descriptor", "SpecError", "GridError"]
