@@ -395,7 +395,9 @@ int launch_box3d_t(sb_plan* P, int src_idx) {
     // rejected: 96-thread CTAs (366-377), a skewed pipeline on mbarriers (390-402),
     // per-die work queues (402), a warp-specialised level split (335); fp32: a split-phase
     // level pipeline (mbarrier arrive after level 1 of plane t, wait before level 2 of plane
-    // t - 1, four level-1 planes: 758 vs 770 -- the CTA barrier is not what bounds it)
+    // t - 1, four level-1 planes: 758 vs 770 -- the CTA barrier is not what bounds it); fp64 on
+    // the 3x-unrolled loop (no role-rotation moves): 64 x 16 tiles at 3 CTAs/SM (158 registers)
+    // 433 vs 440, 64 x 32 at 1 CTA/SM (194 registers) 392, at 2 CTAs/SM it spills (372)
     // (with the guided tail of the z schedule: fp32 3x-unrolled loop 713 -> 761, 64 x 32 tiles
     // 765; fp64 64 x 32 tiles 411 -> 414)
     static const int nw = (int)env_double("SB200_B3_NW", 8);
