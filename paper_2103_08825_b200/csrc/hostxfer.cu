@@ -58,8 +58,10 @@ int host_threads() {
 }  // namespace
 
 // rows x row_bytes from src (pitch sp) to dst (pitch dp), split over the host threads
-void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t row_bytes, size_t rows) {
-    const int nt = (int)std::min<size_t>((size_t)host_threads(), std::max<size_t>(1, rows * row_bytes / (1u << 20)));
+void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t row_bytes, size_t rows, int share) {
+    // `share` > 1: this caller takes 1/share of the host threads (two directions at once)
+    const int cap = std::max(1, host_threads() / std::max(1, share));
+    const int nt = (int)std::min<size_t>((size_t)cap, std::max<size_t>(1, rows * row_bytes / (1u << 20)));
     auto work = [=](int t) {
         if (dp == row_bytes && sp == row_bytes) {      // contiguous: split by bytes (64 B granules)
             const size_t total = rows * row_bytes;

@@ -208,7 +208,10 @@ int guided_z_segments(int64_t z_lo, int64_t nzr, int tiles, int ctas_max, double
     int nb = 0;
     zb[0] = (int)z_lo;
     lmin = std::max<int64_t>(1, lmin);
-    const int64_t neq = std::max<int64_t>(1, std::min<int64_t>(max_seg, (int64_t)(per * ctas_max / tiles + 0.5)));
+    // (short ranges -- a block of a streamed sweep -- in segments of at least 32 planes: each
+    // segment re-computes a 2K-plane warm-up)
+    const int64_t neq = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(max_seg, std::max<int64_t>(1, nzr / 32)),
+                                                              (int64_t)(per * ctas_max / tiles + 0.5)));
     const int64_t lmax = std::max<int64_t>(guide > 0 ? lmin : 1, (nzr + neq - 1) / neq);
     int64_t rem = nzr;
     while (rem > 0) {

@@ -126,7 +126,7 @@ int h2d_pageable_rows(void* dst, const void* host, size_t host_pitch, size_t row
                       cudaStream_t st);
 int d2h_pageable_rows(void* host, size_t host_pitch, const void* src, size_t src_pitch, size_t row_bytes, size_t rows,
                       int device, cudaStream_t st);
-void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t row_bytes, size_t rows);
+void parallel_copy_rows(char* dst, size_t dp, const char* src, size_t sp, size_t row_bytes, size_t rows, int share = 1);
 int xfer_acquire(int device, void* up[2], void* down[2], size_t* chunk_bytes);
 void xfer_release();
 bool sep2d_ok(const sb_plan* P, int k);   // launch2d.cu: separable composed 2D path serves depth k

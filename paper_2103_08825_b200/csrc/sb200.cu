@@ -11,7 +11,10 @@
 
 #include <algorithm>
 #include <cstdarg>
+#include <condition_variable>
 #include <cstdio>
+#include <mutex>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -869,8 +872,11 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
         return f > 0 ? f + r : (int64_t)0;
     };
 
-    struct Dl { int64_t r0, r1; };      // download row ranges, in order
-    std::vector<Dl> dlq;
+    struct Dl { int64_t r0, r1; cudaEvent_t after; };   // download row ranges, in order (`after`: the block's kernels)
+    std::vector<Dl> dlq;                // (guarded by dl_mu: the downloader thread consumes it)
+    std::mutex dl_mu;
+    std::condition_variable dl_cv;
+    bool dl_closed = false;
     size_t dl_issued = 0, dl_drained = 0;
     int64_t dl_planes = 0;              // host planes queued so far
     int dslot_issue = 0, dslot_drain = 0;
@@ -896,47 +902,88 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
         SB_CUDA(cudaEventRecord(done, P->stream));
         const int64_t hp = final_hi(b);
         if (hp > dl_planes) {
-            SB_CUDA(cudaStreamWaitEvent(res.down, done, 0));
-            for (int64_t r0 = dl_planes * R; r0 < hp * R; r0 += rpc) dlq.push_back({r0, std::min(r0 + rpc, hp * R)});
+            {
+                std::lock_guard<std::mutex> g(dl_mu);
+                for (int64_t r0 = dl_planes * R; r0 < hp * R; r0 += rpc)
+                    dlq.push_back({r0, std::min(r0 + rpc, hp * R), r0 == dl_planes * R ? done : nullptr});
+            }
+            dl_cv.notify_one();
             dl_planes = hp;
         }
         return SB_OK;
     };
-    // issue queued D2H chunks into free bounce slots; drain finished ones (all, if `block`)
-    auto pump_downloads = [&](bool block) -> int {
+    // The downloader thread: issues queued D2H chunks into the two bounce slots and copies
+    // finished ones out to the caller's array, until the queue is closed and empty.  (One
+    // thread feeding both directions measured no better than the plain sequence.)
+    int dl_rc = SB_OK;
+    auto downloader = [&]() {
+        if (cudaSetDevice(P->device) != cudaSuccess) {
+            dl_rc = SB_ERR_CUDA;
+            return;
+        }
         for (;;) {
-            while (dl_issued < dlq.size() && dl_issued - dl_drained < 2) {
-                const Dl& d = dlq[dl_issued];
+            size_t avail;
+            {
+                std::unique_lock<std::mutex> g(dl_mu);
+                dl_cv.wait(g, [&] { return dl_closed || dlq.size() > dl_issued || dl_issued > dl_drained; });
+                avail = dlq.size();
+                if (dl_closed && dl_drained == avail) return;
+            }
+            while (dl_issued < avail && dl_issued - dl_drained < 2) {
+                Dl d;
+                {
+                    std::lock_guard<std::mutex> g(dl_mu);
+                    d = dlq[dl_issued];
+                }
                 const char* src = reinterpret_cast<const char*>(P->buf[final_buf]) + P->host_dst_offset * P->es +
                                   (size_t)d.r0 * dpitch;
-                SB_CUDA(cudaMemcpy2DAsync(bdn[dslot_issue], rb, src, dpitch, rb, (size_t)(d.r1 - d.r0),
-                                          cudaMemcpyDeviceToHost, res.down));
-                SB_CUDA(cudaEventRecord(dn_slot[dslot_issue], res.down));
+                if ((d.after && cudaStreamWaitEvent(res.down, d.after, 0) != cudaSuccess) ||
+                    cudaMemcpy2DAsync(bdn[dslot_issue], rb, src, dpitch, rb, (size_t)(d.r1 - d.r0), cudaMemcpyDeviceToHost,
+                                      res.down) != cudaSuccess ||
+                    cudaEventRecord(dn_slot[dslot_issue], res.down) != cudaSuccess) {
+                    dl_rc = SB_ERR_CUDA;
+                    return;
+                }
                 dslot_issue ^= 1;
                 dl_issued++;
             }
-            if (dl_drained == dl_issued) return SB_OK;
-            if (!block) {
-                const cudaError_t q = cudaEventQuery(dn_slot[dslot_drain]);
-                if (q == cudaErrorNotReady) return SB_OK;
-                if (q != cudaSuccess) return fail(SB_ERR_CUDA, "download failed: %s", cudaGetErrorString(q));
-            } else {
-                SB_CUDA(cudaEventSynchronize(dn_slot[dslot_drain]));
+            if (dl_drained < dl_issued) {
+                if (cudaEventSynchronize(dn_slot[dslot_drain]) != cudaSuccess) {
+                    dl_rc = SB_ERR_CUDA;
+                    return;
+                }
+                Dl d;
+                {
+                    std::lock_guard<std::mutex> g(dl_mu);
+                    d = dlq[dl_drained];
+                }
+                sbh::parallel_copy_rows(out + (size_t)d.r0 * out_pitch, out_pitch,
+                                        static_cast<const char*>(bdn[dslot_drain]), rb, rb, (size_t)(d.r1 - d.r0), 2);
+                dslot_drain ^= 1;
+                dl_drained++;
             }
-            const Dl& d = dlq[dl_drained];
-            sbh::parallel_copy_rows(out + (size_t)d.r0 * out_pitch, out_pitch, static_cast<const char*>(bdn[dslot_drain]),
-                                    rb, rb, (size_t)(d.r1 - d.r0));
-            dslot_drain ^= 1;
-            dl_drained++;
         }
     };
+    std::thread dl_thread(downloader);
+    auto finish_downloads = [&]() {     // close the queue and wait for the thread (every exit path)
+        {
+            std::lock_guard<std::mutex> g(dl_mu);
+            dl_closed = true;
+        }
+        dl_cv.notify_one();
+        if (dl_thread.joinable()) dl_thread.join();
+    };
+    struct Joiner {
+        decltype(finish_downloads)& f;
+        ~Joiner() { f(); }
+    } joiner{finish_downloads};
 
     // ---- upload chunks; blocks are enqueued as their planes arrive
     for (int64_t c = 0; c < nchunks; c++) {
         const int slot = (int)(c & 1);
         const int64_t r0 = c * rpc, nr = std::min(rpc, rows - r0);
         SB_CUDA(cudaEventSynchronize(up_slot[slot]));
-        sbh::parallel_copy_rows(static_cast<char*>(bup[slot]), rb, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr);
+        sbh::parallel_copy_rows(static_cast<char*>(bup[slot]), rb, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr, 2);
         SB_CUDA(cudaMemcpy2DAsync(b0 + (size_t)r0 * dpitch, dpitch, bup[slot], rb, rb, (size_t)nr, cudaMemcpyHostToDevice,
                                   res.up));
         SB_CUDA(cudaEventRecord(up_slot[slot], res.up));
@@ -951,10 +998,10 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
             while (next_block < nblocks && have >= need_rows(next_block))
                 if ((rc = enqueue_block(next_block++, uploaded)) != SB_OK) return rc;
         }
-        if ((rc = pump_downloads(false)) != SB_OK) return rc;
     }
     P->uploaded = true;
-    if ((rc = pump_downloads(true)) != SB_OK) return rc;
+    finish_downloads();
+    if (dl_rc != SB_OK) return fail(dl_rc, "streamed download failed: %s", cudaGetErrorString(cudaGetLastError()));
     P->cur = final_buf;
     P->zr_lo = 0;
     P->zr_hi = -1;
@@ -986,9 +1033,9 @@ int sb_sweep_host(sb_plan* P, const void* host_in, size_t in_pitch, void* host_o
             done += kk;
         }
     }
-    // Opt-in (read per call): measured on the C5 box 412 vs 464 ms per call with 8 blocks, but
-    // on C4 (T = 200: 100 launches + their shell kernels per block) 201 vs 133 ms -- one host
-    // thread feeds both directions and 8 x L small range launches cost more than they hide.
+    // Opt-in (read per call): measured on the C5 box 320-335 vs 347 ms per call with 8 blocks, on
+    // C4 (T = 200: 100 launches + their shell kernels per block) 168-202 vs 133 ms -- the host
+    // copies (the box crosses the CPU twice) bound the call, not the missing overlap.
     const int enabled = (int)env_double("SB200_STREAM_SWEEP", 0);
     const int nblocks_env = (int)env_double("SB200_STREAM_BLOCKS", 8);
     const int64_t n = P->dims[0];
