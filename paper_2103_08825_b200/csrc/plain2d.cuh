@@ -20,9 +20,10 @@
 //    shuffles (levels >= 2) or four shared loads (level 1) plus the push;
 //  * staging by whole 32 B sectors: instruction c of a row copies columns
 //    [64c, 64c + 64) with lane L on 16 B chunk L, so a warp instruction reads
-//    16 full sectors (fused2d_kernel's lane-owned 32 B chunks read half of 32
-//    sectors per instruction: 2x the L2 -> SM sector traffic); the two
-//    strip-edge halo columns are one 16 B chunk each (lanes 0, 1);
+//    16 full sectors (fused2d_item's lane-owned 32 B chunks touch half of 32
+//    sectors per instruction; measured L2 traffic per C3b launch 11.1 -> 10.8
+//    GB, so the coalescer already merged most of that); the two strip-edge
+//    halo columns are one 16 B chunk each (lanes 0, 1);
 //  * level 1 reads its x-neighbours from the shared row, not by shuffles
 //    (the strip-edge lanes need no select);
 //  * ring of 9 rows, prefetch distance 8; the row loop is unrolled x3 (the
