@@ -550,9 +550,14 @@ def run_gpu_arm(args):
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            upload()
-            run_once()
-            download()
+            if world == 1:
+                # the one-call form of upload + T steps + download (sb_sweep_host; pinned buffers:
+                # on 3D plans the transfers stream block by block beside the sweep)
+                plan.sweep_host(host_in.numpy(), T, out=host_out.numpy())
+            else:
+                upload()
+                run_once()
+                download()
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         tt = torch.tensor([dt], device="cpu" if dist is not None and dist.get_backend() == "gloo" else "cuda")
@@ -563,7 +568,8 @@ def run_gpu_arm(args):
         e2e = {"value": serial, "unit": "GStencil/s",
                "h2d_bytes_per_step": int(host_in.numel() * es * world),
                "d2h_bytes_per_step": int(host_out.numel() * es * world),
-               "mode": "serial", "timer": "host wall clock around upload+sweep+download, max over ranks"}
+               "mode": "serial", "timer": "host wall clock around upload+sweep+download (N=1: one sb_sweep_host "
+                                          "call per step), max over ranks"}
         grid_bytes = host_in.numel() * es
         if world == 1:
             want = host_out.numpy().copy()                       # serial result of the last step

@@ -128,10 +128,10 @@ int sb_upload_pitched(sb_plan *plan, const void *host, size_t pitch_bytes);
 int sb_download_pitched(sb_plan *plan, void *host, size_t pitch_bytes);
 
 /* Host box in, `steps` steps, host box out (pitches as above; 0 = compact rows;
- * in and out may be the same memory): upload, run, download in one call.  With
- * SB200_STREAM_SWEEP=1 (opt-in, measured a gain only for few-launch sweeps) 3D
- * whole-grid plans overlap the transfers with the sweep: the grid is cut into
- * blocks of planes, every launch
+ * in and out may be the same memory): upload, run, download in one call.  3D
+ * whole-grid plans can overlap the transfers with the sweep (default with pinned
+ * host memory on both sides and few launches; SB200_STREAM_SWEEP=1/0 forces it
+ * on / off): the grid is cut into blocks of planes, every launch
  * of the sweep runs block by block on ranges shifted down by the reach of the
  * launches before it, so a block's launches start once its planes have arrived
  * and its final planes travel back while later blocks compute -- the same range

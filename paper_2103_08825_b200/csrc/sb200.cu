@@ -839,11 +839,17 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
     std::vector<int64_t> S(L + 1, 0);
     for (int j = 0; j < L; j++) S[j + 1] = S[j] + r * ks[j];
     StreamRes res;
-    void *bup[2], *bdn[2];
-    size_t chunk = 0;
-    int rc = sbh::xfer_acquire(P->device, bup, bdn, &chunk);
-    if (rc != SB_OK) return rc;
-    res.locked = true;
+    // pinned host memory is read / written by the copy engines directly; pageable memory goes
+    // through the bounce buffers with host copy threads (hostxfer.cu)
+    const bool pin_in = sbh::host_is_pinned(in), pin_out = sbh::host_is_pinned(out);
+    void *bup[2] = {nullptr, nullptr}, *bdn[2] = {nullptr, nullptr};
+    size_t chunk = (size_t)32 << 20;
+    int rc = SB_OK;
+    if (!pin_in || !pin_out) {
+        rc = sbh::xfer_acquire(P->device, bup, bdn, &chunk);
+        if (rc != SB_OK) return rc;
+        res.locked = true;
+    }
     SB_CUDA(cudaStreamCreateWithFlags(&res.up, cudaStreamNonBlocking));
     SB_CUDA(cudaStreamCreateWithFlags(&res.down, cudaStreamNonBlocking));
     const int64_t rows = P->host_rows;
@@ -929,7 +935,7 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
                 avail = dlq.size();
                 if (dl_closed && dl_drained == avail) return;
             }
-            while (dl_issued < avail && dl_issued - dl_drained < 2) {
+            while (dl_issued < avail && (pin_out || dl_issued - dl_drained < 2)) {
                 Dl d;
                 {
                     std::lock_guard<std::mutex> g(dl_mu);
@@ -937,6 +943,17 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
                 }
                 const char* src = reinterpret_cast<const char*>(P->buf[final_buf]) + P->host_dst_offset * P->es +
                                   (size_t)d.r0 * dpitch;
+                if (pin_out) {          // straight into the caller's rows; the stream is synchronised at the end
+                    if ((d.after && cudaStreamWaitEvent(res.down, d.after, 0) != cudaSuccess) ||
+                        cudaMemcpy2DAsync(out + (size_t)d.r0 * out_pitch, out_pitch, src, dpitch, rb, (size_t)(d.r1 - d.r0),
+                                          cudaMemcpyDeviceToHost, res.down) != cudaSuccess) {
+                        dl_rc = SB_ERR_CUDA;
+                        return;
+                    }
+                    dl_issued++;
+                    dl_drained++;
+                    continue;
+                }
                 if ((d.after && cudaStreamWaitEvent(res.down, d.after, 0) != cudaSuccess) ||
                     cudaMemcpy2DAsync(bdn[dslot_issue], rb, src, dpitch, rb, (size_t)(d.r1 - d.r0), cudaMemcpyDeviceToHost,
                                       res.down) != cudaSuccess ||
@@ -958,7 +975,7 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
                     d = dlq[dl_drained];
                 }
                 sbh::parallel_copy_rows(out + (size_t)d.r0 * out_pitch, out_pitch,
-                                        static_cast<const char*>(bdn[dslot_drain]), rb, rb, (size_t)(d.r1 - d.r0), 2);
+                                        static_cast<const char*>(bdn[dslot_drain]), rb, rb, (size_t)(d.r1 - d.r0), pin_in ? 1 : 2);
                 dslot_drain ^= 1;
                 dl_drained++;
             }
@@ -982,11 +999,17 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
     for (int64_t c = 0; c < nchunks; c++) {
         const int slot = (int)(c & 1);
         const int64_t r0 = c * rpc, nr = std::min(rpc, rows - r0);
-        SB_CUDA(cudaEventSynchronize(up_slot[slot]));
-        sbh::parallel_copy_rows(static_cast<char*>(bup[slot]), rb, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr, 2);
-        SB_CUDA(cudaMemcpy2DAsync(b0 + (size_t)r0 * dpitch, dpitch, bup[slot], rb, rb, (size_t)nr, cudaMemcpyHostToDevice,
-                                  res.up));
-        SB_CUDA(cudaEventRecord(up_slot[slot], res.up));
+        if (pin_in) {
+            SB_CUDA(cudaMemcpy2DAsync(b0 + (size_t)r0 * dpitch, dpitch, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr,
+                                      cudaMemcpyHostToDevice, res.up));
+        } else {
+            SB_CUDA(cudaEventSynchronize(up_slot[slot]));
+            sbh::parallel_copy_rows(static_cast<char*>(bup[slot]), rb, in + (size_t)r0 * in_pitch, in_pitch, rb, (size_t)nr,
+                                    pin_out ? 1 : 2);
+            SB_CUDA(cudaMemcpy2DAsync(b0 + (size_t)r0 * dpitch, dpitch, bup[slot], rb, rb, (size_t)nr,
+                                      cudaMemcpyHostToDevice, res.up));
+            SB_CUDA(cudaEventRecord(up_slot[slot], res.up));
+        }
         // the halo / ghost cells live in both buffers (kernels never write them)
         SB_CUDA(cudaMemcpy2DAsync(b1 + (size_t)r0 * dpitch, dpitch, b0 + (size_t)r0 * dpitch, dpitch, rb, (size_t)nr,
                                   cudaMemcpyDeviceToDevice, res.up));
@@ -1002,6 +1025,7 @@ int stream_sweep_t(sb_plan* P, const char* in, size_t in_pitch, char* out, size_
     P->uploaded = true;
     finish_downloads();
     if (dl_rc != SB_OK) return fail(dl_rc, "streamed download failed: %s", cudaGetErrorString(cudaGetLastError()));
+    SB_CUDA(cudaStreamSynchronize(res.down));
     P->cur = final_buf;
     P->zr_lo = 0;
     P->zr_hi = -1;
@@ -1033,11 +1057,17 @@ int sb_sweep_host(sb_plan* P, const void* host_in, size_t in_pitch, void* host_o
             done += kk;
         }
     }
-    // Opt-in (read per call): measured on the C5 box 320-335 vs 347 ms per call with 8 blocks, on
-    // C4 (T = 200: 100 launches + their shell kernels per block) 168-202 vs 133 ms -- the host
-    // copies (the box crosses the CPU twice) bound the call, not the missing overlap.
-    const int enabled = (int)env_double("SB200_STREAM_SWEEP", 0);
+    // Pageable memory: opt-in (SB200_STREAM_SWEEP=1, read per call).  Measured on the C5 box
+    // 320-335 vs 347 ms per call with 8 blocks, on C4 (T = 200: 100 launches + their shell
+    // kernels per block) 168-202 vs 133 ms -- the host copies (the box crosses the CPU twice)
+    // bound the call, not the missing overlap.
     const int nblocks_env = (int)env_double("SB200_STREAM_BLOCKS", 8);
+    // With PINNED memory on both sides there are no host copies and the streamed form is the
+    // default when the sweep is few launches (SB200_STREAM_SWEEP unset; 0 / 1 force it).
+    const int mode = (int)env_double("SB200_STREAM_SWEEP", -1);
+    const bool enabled = mode > 0 || (mode < 0 && ks.size() * (size_t)nblocks_env <= 512 &&
+                                      sbh::host_is_pinned(host_in) && sbh::host_is_pinned(host_out));
+
     const int64_t n = P->dims[0];
     const int64_t shift = ks.empty() ? 0 : (int64_t)P->r * (steps - ks.back());
     const int nblocks = (int)std::max<int64_t>(1, std::min<int64_t>(nblocks_env, n / std::max<int64_t>(1, 4 * P->r * (ks.empty() ? 1 : ks[0]))));

@@ -100,3 +100,28 @@ def test_long_sweep_falls_back_when_the_shift_exceeds_the_grid():
         want = plain(p, box, 140)
         got = p.sweep_host(box, 140)
     assert got.tobytes() == want.tobytes()
+
+
+def test_streamed_pinned_memory_direct(monkeypatch):
+    # pinned host memory on both sides: the copy engines read / write the caller's rows
+    # directly (no bounce buffers) and streaming is the default for few-launch sweeps
+    torch = pytest.importorskip("torch")
+    monkeypatch.delenv("SB200_STREAM_SWEEP", raising=False)
+    spec = config_spec("c5")
+    box = seeded_box(BIG, 1, seed=33)
+    pin_in = torch.empty(box.shape, dtype=torch.float64, pin_memory=True)
+    pin_in.numpy()[...] = box
+    pin_out = torch.empty_like(pin_in, pin_memory=True)
+    with Plan(spec, BIG, arith="exact") as p:
+        want = plain(p, box, 6)
+        p.sweep_host(pin_in.numpy(), 6, out=pin_out.numpy())
+        assert pin_out.numpy().tobytes() == want.tobytes()
+        # in place, and mixed pinned / pageable
+        p.sweep_host(pin_in.numpy(), 6, out=pin_in.numpy())
+        assert pin_in.numpy().tobytes() == want.tobytes()
+        monkeypatch.setenv("SB200_STREAM_SWEEP", "1")
+        pin_in.numpy()[...] = box
+        got = p.sweep_host(pin_in.numpy(), 6)
+        assert got.tobytes() == want.tobytes()
+        got2 = p.sweep_host(box, 6, out=pin_out.numpy())
+        assert got2.tobytes() == want.tobytes()
