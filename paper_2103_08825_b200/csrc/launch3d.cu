@@ -209,7 +209,9 @@ int guided_z_segments(int64_t z_lo, int64_t nzr, int tiles, int ctas_max, double
     zb[0] = (int)z_lo;
     lmin = std::max<int64_t>(1, lmin);
     // (short ranges -- a block of a streamed sweep -- in segments of at least 32 planes: each
-    // segment re-computes a 2K-plane warm-up)
+    // segment re-computes a 2K-plane warm-up.  One segment per tile for a 96-plane block --
+    // best by CTA fill x warm-up overhead, 0.93 vs ~0.80 -- measured slower, streamed C5
+    // sweep 171 vs 156 ms, fp32 146 vs 116: long items let the tiles drift apart in z)
     const int64_t neq = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(max_seg, std::max<int64_t>(1, nzr / 32)),
                                                               (int64_t)(per * ctas_max / tiles + 0.5)));
     const int64_t lmax = std::max<int64_t>(guide > 0 ? lmin : 1, (nzr + neq - 1) / neq);
